@@ -1,0 +1,169 @@
+/*
+ * graphlet_b200.h -- C-ABI of the B200-native edge-centric k<=4 graphlet
+ * counter (arxiv 1608.05138).  Plain pointers and sizes only; no torch or CUDA
+ * types cross this boundary (streams are passed as void*).
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/include/graphlet/*.hpp); see INTEGRATION.md for the
+ * binding a maintainer of the reference would add.
+ *
+ * Error behaviour mirrors the reference's exception classes: every function
+ * returns GL_OK (0) or a negative code, and gl_last_error() holds the message
+ * (thread-local).  parse errors additionally report the 1-based line number
+ * through gl_last_error_line(), like graphlet::parse_error::line().
+ */
+#ifndef GRAPHLET_B200_H
+#define GRAPHLET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (reference exception class in parentheses) ---- */
+#define GL_OK 0
+#define GL_ERR_INVALID -1     /* std::invalid_argument                              */
+#define GL_ERR_PARSE -2       /* graphlet::parse_error           (graph.hpp:23-33)  */
+#define GL_ERR_IO -3          /* std::runtime_error "cannot open" (graph.cpp:87-91) */
+#define GL_ERR_CUDA -4        /* device failure / no CUDA device / ext. missing      */
+#define GL_ERR_CONSISTENCY -5 /* graphlet::count_consistency_error (counts.hpp:13-16)*/
+#define GL_ERR_OVERFLOW -6    /* graphlet::count_overflow_error, 32-bit id space     */
+#define GL_ERR_OOM -7         /* device allocation failed                           */
+#define GL_ERR_STATE -8       /* call sequence violated (e.g. finish before begin)  */
+
+const char *gl_last_error(void);
+uint64_t gl_last_error_line(void);
+const char *gl_version(void);
+
+/* 128-bit unsigned count, little-endian limbs (count_t, common.hpp:17). */
+typedef struct {
+    uint64_t lo, hi;
+} gl_u128;
+
+/* Global counts X_0..X_17, X[0] unused (GraphletVector, counts.hpp:55-61). */
+typedef struct {
+    gl_u128 x[18];
+} gl_graphlet_vector;
+
+/* Unrestricted sums C_0..C_16, indices 3..5 and 7..16 used
+ * (UnrestrictedCounts, counts.hpp:41-47). */
+typedef struct {
+    gl_u128 c[17];
+} gl_unrestricted;
+
+/* Per-edge micro record, field-for-field the reference MicroRecord
+ * (counts.hpp:82-89) widened to 64-bit edge ids. */
+typedef struct {
+    uint64_t edge_id, x3, x4, x5, x7, x10, t, s_u, s_v, d_e;
+} gl_micro_record;
+
+/* ------------------------------------------------------------------ input */
+
+/* Parse a text edge list held in memory (load_edge_list, graph.hpp:38;
+ * graph.cpp:47-85): '#'/'%' comments, a %%MatrixMarket banner skips the next
+ * dimension line, two unsigned integer tokens per data line.  On success
+ * *pairs is a malloc'd array of 2*count labels (a0,b0,a1,b1,...) to be freed
+ * with gl_free(); an empty input yields count 0. */
+int gl_load_edge_list(const char *text, size_t len, uint64_t **pairs, uint64_t *count);
+/* load_edge_list_file (graph.hpp:39; graph.cpp:87-91). */
+int gl_load_edge_list_file(const char *path, uint64_t **pairs, uint64_t *count);
+void gl_free(void *p);
+
+/* Deterministic synthetic generators (SPEC cli "built-in deterministic
+ * generator"); host output, 2*count labels.  RMAT uses Graph500 quadrant
+ * probabilities given as a,b,c (d = 1-a-b-c) and a counter-based hash, so
+ * gl_generate_rmat_device() produces the identical list directly in HBM. */
+int gl_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                     uint64_t seed, uint64_t **pairs, uint64_t *count);
+int gl_generate_rmat_device(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                            uint64_t seed, int device, uint64_t *d_pairs /* 2*count */,
+                            uint64_t count);
+/* Erdos-Renyi G(n, m): exactly m distinct non-loop edges. */
+int gl_generate_gnm(uint64_t n, uint64_t m, uint64_t seed, uint64_t **pairs, uint64_t *count);
+/* Barabasi-Albert: n vertices, each new vertex attaches `attach` edges. */
+int gl_generate_ba(uint64_t n, uint32_t attach, uint64_t seed, uint64_t **pairs, uint64_t *count);
+
+/* ------------------------------------------------------------------ graph */
+
+typedef struct gl_graph gl_graph; /* device-resident preprocessed graph */
+
+/* build_graph (graph.hpp:96; graph.cpp:93-172) executed on `device`:
+ * label compaction, self-loop and duplicate removal, P1 relabel by
+ * (degree asc, label asc), id-sorted CSR rows, oriented edge ids identical to
+ * orient_edges (graph.cpp:180-193).  `pairs` is a HOST array of 2*count labels. */
+int gl_graph_build(const uint64_t *pairs, uint64_t count, int device, gl_graph **out);
+/* Same, `d_pairs` already in device memory on `device` (not modified). */
+int gl_graph_build_device(const uint64_t *d_pairs, uint64_t count, int device, gl_graph **out);
+void gl_graph_free(gl_graph *g);
+
+uint64_t gl_graph_num_vertices(const gl_graph *g); /* Graph::num_vertices */
+uint64_t gl_graph_num_edges(const gl_graph *g);    /* Graph::num_edges    */
+uint32_t gl_graph_max_degree(const gl_graph *g);   /* Graph::max_degree   */
+/* Host copies: degree[n] (Graph::degree), label[n] (Graph::original_label),
+ * offsets[n+1] and adjacency[2m] (Graph::neighbors_by_id rows). */
+int gl_graph_degrees(const gl_graph *g, uint32_t *degree);
+int gl_graph_labels(const gl_graph *g, uint64_t *label);
+int gl_graph_csr(const gl_graph *g, uint64_t *offsets, uint32_t *adjacency);
+/* orient_edges (graph.hpp:107): internal ids of (v = high, u = low) per edge id. */
+int gl_orient_edges(const gl_graph *g, uint32_t *v, uint32_t *u);
+
+/* ------------------------------------------------------------- counting */
+
+/* Count all 2/3/4-vertex graphlets, macro and micro, on the graph's device.
+ * Replaces the reference's per-edge loop process_edge_hash/_bsearch
+ * (kernels.hpp:99-102) + accumulate_unrestricted + merge
+ * (counts.hpp:49-51) + global_from_unrestricted (counts.hpp:69-70).
+ * `unres` may be NULL.  Per-edge results stay resident on the device for
+ * gl_micro_* below. */
+int gl_count(gl_graph *g, gl_graphlet_vector *X, gl_unrestricted *unres);
+
+/* Sharded form for one process per GPU:
+ *  1. gl_count_begin: every rank computes the full per-edge triangle counts,
+ *     then its cost-balanced share (rank of world) of the clique and cycle
+ *     work, leaving per-edge int64 partials in `d_partials` (device memory of
+ *     2*gl_partials_len(g, world) int64, zeroed by the callee).
+ *  2. caller sums d_partials across ranks (reduce-scatter or all-reduce,
+ *     e.g. NCCL), so that rank r holds the summed rows of edges
+ *     [edge_begin, edge_end) at d_partials[2*edge_begin ...].
+ *  3. gl_count_finish: per-edge epilogue for that shard, micro records on
+ *     device, unrestricted partial sums returned in *unres.
+ *  4. caller sums unres across ranks (e.g. as 32-bit limbs in int64) and
+ *     calls gl_global_from_unrestricted. */
+uint64_t gl_partials_len(const gl_graph *g, int world);
+int gl_count_begin(gl_graph *g, int rank, int world, int64_t *d_partials, void *stream);
+int gl_count_finish(gl_graph *g, const int64_t *d_partials, uint64_t edge_begin,
+                    uint64_t edge_end, gl_unrestricted *unres, void *stream);
+
+/* global_from_unrestricted (counts.cpp:86-111), host-side 128-bit algebra.
+ * GL_ERR_CONSISTENCY on an inexact division or a negative intermediate. */
+int gl_global_from_unrestricted(const gl_unrestricted *c, uint64_t n, uint64_t m,
+                                gl_graphlet_vector *X);
+
+/* micro_counts (counts.hpp:90; counts.cpp:122-136) for edge ids
+ * [first, first+count) of the last gl_count / gl_count_finish shard. */
+int gl_micro_records(const gl_graph *g, uint64_t first, uint64_t count, gl_micro_record *out);
+/* Compact per-edge output (SoA, host): t, x7, x10 for edge ids
+ * [first, first+count); any pointer may be NULL.  The other MicroRecord
+ * fields are closed-form in (t, deg(u), deg(v), n) -- counts.cpp:113-136. */
+int gl_edge_counts(const gl_graph *g, uint64_t first, uint64_t count, uint32_t *t, uint64_t *x7,
+                   uint64_t *x10);
+/* Device pointers of the resident per-edge arrays (t: uint32[m], x7 and x10:
+ * uint64[m]); valid until the next count call or gl_graph_free. */
+int gl_edge_counts_device(const gl_graph *g, const uint32_t **t, const uint64_t **x7,
+                          const uint64_t **x10);
+
+/* Kernel timing of the last count call (CUDA events on the launching stream),
+ * milliseconds: [0] triangles, [1] cliques+triangle-sums, [2] cycles,
+ * [3] epilogue+macro reduction, [4] total.  Launch count in *launches. */
+int gl_last_timings(const gl_graph *g, float ms[5], uint32_t *launches);
+/* Algorithmic work counters of the last count call:
+ * [0] adjacency entries read by the triangle kernel, [1] by the clique
+ * kernel, [2] by the cycle kernel, [3] edges finalised. */
+int gl_last_work(const gl_graph *g, uint64_t work[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPHLET_B200_H */

@@ -1,0 +1,379 @@
+// build.cu -- on-device CSR build: the B200 counterpart of graphlet::build_graph
+// (/root/reference/proj/src/graph.cpp:93-172) and orient_edges (:180-193).
+//
+// Every step is a sort, a scan or a bandwidth-bound elementwise pass:
+//   1. label universe: radix-sort all 2*count endpoint labels, unique -> n
+//      (self-loop endpoints stay vertices, as in the reference)
+//   2. compact + canonicalise (min,max) into one u64 key, drop loops, radix
+//      sort, unique -> m simple undirected edges
+//   3. degrees; P1 relabel by (degree asc, label asc) = radix sort of
+//      (deg<<32 | compact id) -- compact ids are already label-ordered
+//   4. both directions of every edge as (src<<32 | dst) keys, radix sort ->
+//      id-sorted rows (the reference's neighbors_by_id view)
+//   5. lcnt/loff/eid/ev/eu/epos: the oriented edge id of each slot is its rank
+//      in the lower prefix of the high endpoint's row, exactly the
+//      reference's ascending-(v,u) enumeration.
+// The reference's degree-descending iteration view (adj_deg_) only orders
+// the reference's loops; counts do not depend on it, so it is not built.
+#include <cub/cub.cuh>
+
+#include "graph.cuh"
+
+namespace gl {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(u64 n, int threads = kThreads) {
+    u64 g = (n + threads - 1) / threads;
+    if (g == 0) g = 1;
+    if (g > 148ull * 64) g = 148ull * 64; // grid-stride beyond ~64 waves
+    return (unsigned)g;
+}
+
+inline int bits_for(u64 x) { // number of bits to represent values <= x
+    int b = 0;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return b == 0 ? 1 : b;
+}
+
+struct CubTemp {
+    DevBuf buf;
+    void* ensure(size_t b) {
+        buf.alloc(b);
+        return buf.p;
+    }
+};
+
+template <typename K>
+void sort_keys(CubTemp& tmp, K* in, K* out, u64 n, int end_bit, cudaStream_t s) {
+    size_t bytes = 0;
+    GL_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, (int64_t)n, 0, end_bit, s));
+    void* t = tmp.ensure(bytes);
+    GL_CUDA(cub::DeviceRadixSort::SortKeys(t, bytes, in, out, (int64_t)n, 0, end_bit, s));
+}
+
+template <typename K>
+u64 unique_keys(CubTemp& tmp, const K* in, K* out, u64 n, u64* d_count, cudaStream_t s) {
+    size_t bytes = 0;
+    GL_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, in, out, d_count, (int64_t)n, s));
+    void* t = tmp.ensure(bytes);
+    GL_CUDA(cub::DeviceSelect::Unique(t, bytes, in, out, d_count, (int64_t)n, s));
+    u64 h = 0;
+    GL_CUDA(cudaMemcpyAsync(&h, d_count, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    GL_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+template <typename T>
+void exclusive_scan(CubTemp& tmp, const T* in, T* out, u64 n, cudaStream_t s) {
+    size_t bytes = 0;
+    GL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, s));
+    void* t = tmp.ensure(bytes);
+    GL_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, (int64_t)n, s));
+}
+
+__global__ void k_max_label(const u64* __restrict__ p, u64 n, unsigned long long* out) {
+    u64 mx = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        mx = p[i] > mx ? p[i] : mx;
+    for (int d = 16; d > 0; d >>= 1) {
+        u64 o = __shfl_down_sync(0xffffffffu, mx, d);
+        mx = o > mx ? o : mx;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)mx);
+}
+
+// compact both endpoints by binary search in the unique label array
+__global__ void k_edge_keys(const u64* __restrict__ pairs, u64 count, const u64* __restrict__ labels,
+                            u64 n, u64 sentinel, u64* __restrict__ keys) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
+        u64 a = pairs[2 * i], b = pairs[2 * i + 1];
+        if (a == b) {
+            keys[i] = sentinel;
+            continue;
+        }
+        u64 x = lower_bound_dev<u64, u64>(labels, 0, n, a);
+        u64 y = lower_bound_dev<u64, u64>(labels, 0, n, b);
+        if (x > y) {
+            u64 t = x;
+            x = y;
+            y = t;
+        }
+        keys[i] = (x << 32) | y;
+    }
+}
+
+__global__ void k_degree(const u64* __restrict__ keys, u64 m, u32* __restrict__ deg) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+        u64 k = keys[i];
+        atomicAdd(&deg[k >> 32], 1u);
+        atomicAdd(&deg[k & 0xffffffffu], 1u);
+    }
+}
+
+__global__ void k_order_keys(const u32* __restrict__ deg, u64 n, u64* __restrict__ ok) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        ok[i] = ((u64)deg[i] << 32) | i;
+}
+
+__global__ void k_relabel(const u64* __restrict__ sorted_ok, u64 n, const u64* __restrict__ labels,
+                          u32* __restrict__ new_id, u32* __restrict__ deg_new,
+                          u64* __restrict__ label_new) {
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < n; r += (u64)gridDim.x * blockDim.x) {
+        u64 k = sorted_ok[r];
+        u32 old = (u32)(k & 0xffffffffu);
+        new_id[old] = (u32)r;
+        deg_new[r] = (u32)(k >> 32);
+        label_new[r] = labels[old];
+    }
+}
+
+__global__ void k_directed(const u64* __restrict__ keys, u64 m, const u32* __restrict__ new_id,
+                           u64* __restrict__ dir) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+        u64 k = keys[i];
+        u64 a = new_id[k >> 32], b = new_id[k & 0xffffffffu];
+        dir[2 * i] = (a << 32) | b;
+        dir[2 * i + 1] = (b << 32) | a;
+    }
+}
+
+__global__ void k_adj_from_dir(const u64* __restrict__ dir, u64 len, u32* __restrict__ adj) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < len; i += (u64)gridDim.x * blockDim.x)
+        adj[i] = (u32)(dir[i] & 0xffffffffu);
+}
+
+__global__ void k_widen(const u32* __restrict__ a, u64 n, u64* __restrict__ b) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+__global__ void k_lcnt(const u64* __restrict__ off, const u32* __restrict__ adj, u64 n,
+                       u32* __restrict__ lcnt, u64* __restrict__ lcnt64) {
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < n; v += (u64)gridDim.x * blockDim.x) {
+        u64 lo = off[v], hi = off[v + 1];
+        u64 p = lower_bound_dev<u32, u64>(adj, lo, hi, (u32)v);
+        lcnt[v] = (u32)(p - lo);
+        lcnt64[v] = p - lo;
+    }
+}
+
+__global__ void k_slots(const u64* __restrict__ dir, u64 len, const u64* __restrict__ off,
+                        const u32* __restrict__ adj, const u32* __restrict__ lcnt,
+                        const u64* __restrict__ loff, u32* __restrict__ eid, u32* __restrict__ ev,
+                        u32* __restrict__ eu, u32* __restrict__ epos) {
+    for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < len; j += (u64)gridDim.x * blockDim.x) {
+        u32 v = (u32)(dir[j] >> 32);
+        u32 x = adj[j];
+        u64 pos = j - off[v];
+        if (x < v) {
+            u64 e = loff[v] + pos;
+            eid[j] = (u32)e;
+            ev[e] = v;
+            eu[e] = x;
+        } else {
+            u64 lo = off[x];
+            u64 p = lower_bound_dev<u32, u64>(adj, lo, lo + lcnt[x], v);
+            u64 e = loff[x] + (p - lo);
+            eid[j] = (u32)e;
+            epos[e] = (u32)pos;
+        }
+    }
+}
+
+__global__ void k_dmax(const u32* __restrict__ deg, u64 n, unsigned* out) {
+    u32 mx = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        mx = deg[i] > mx ? deg[i] : mx;
+    for (int d = 16; d > 0; d >>= 1) {
+        u32 o = __shfl_down_sync(0xffffffffu, mx, d);
+        mx = o > mx ? o : mx;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+} // namespace
+
+Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
+    GL_CUDA(cudaSetDevice(device));
+    auto* g = new Graph;
+    try {
+        g->device = device;
+        GL_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        cudaStream_t s = g->stream;
+        CubTemp tmp;
+        DevBuf d_cnt;
+        d_cnt.alloc(16);
+        u64* cnt = d_cnt.as<u64>();
+
+        // 1. label universe
+        DevBuf lab_a, lab_b;
+        u64 nlab = 2 * count;
+        lab_a.alloc(nlab * sizeof(u64));
+        lab_b.alloc(nlab * sizeof(u64));
+        u64 n = 0;
+        if (count > 0) {
+            GL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u64), s));
+            k_max_label<<<grid_for(nlab), kThreads, 0, s>>>(d_pairs, nlab, (unsigned long long*)cnt);
+            GL_LAUNCH_CHECK();
+            u64 maxlab = 0;
+            GL_CUDA(cudaMemcpyAsync(&maxlab, cnt, sizeof(u64), cudaMemcpyDeviceToHost, s));
+            GL_CUDA(cudaStreamSynchronize(s));
+            sort_keys<u64>(tmp, const_cast<u64*>(d_pairs), lab_b.as<u64>(), nlab, bits_for(maxlab), s);
+            n = unique_keys<u64>(tmp, lab_b.as<u64>(), lab_a.as<u64>(), nlab, cnt, s);
+        }
+        if (n >= 0xffffffffull) throw overflow_error("graph exceeds 32-bit vertex id space");
+        lab_b.reset();
+        const u64* labels = lab_a.as<u64>();
+        const int vb = bits_for(n ? n - 1 : 0);
+
+        // 2. canonical undirected keys
+        DevBuf keys_a, keys_b;
+        keys_a.alloc((count + 1) * sizeof(u64));
+        keys_b.alloc((count + 1) * sizeof(u64));
+        const u64 sentinel = ((((u64)1 << vb) - 1) << 32) | 0xffffffffull;
+        u64 m = 0;
+        if (count > 0) {
+            k_edge_keys<<<grid_for(count), kThreads, 0, s>>>(d_pairs, count, labels, n, sentinel,
+                                                               keys_a.as<u64>());
+            GL_LAUNCH_CHECK();
+            sort_keys<u64>(tmp, keys_a.as<u64>(), keys_b.as<u64>(), count, 32 + vb, s);
+            u64 nu = unique_keys<u64>(tmp, keys_b.as<u64>(), keys_a.as<u64>(), count, cnt, s);
+            u64 last = 0;
+            if (nu > 0) {
+                GL_CUDA(cudaMemcpyAsync(&last, keys_a.as<u64>() + nu - 1, sizeof(u64),
+                                        cudaMemcpyDeviceToHost, s));
+                GL_CUDA(cudaStreamSynchronize(s));
+            }
+            m = (nu > 0 && last == sentinel) ? nu - 1 : nu;
+        }
+        if (m >= 0xffffffffull) throw overflow_error("graph exceeds 32-bit edge id space");
+        keys_b.reset();
+        const u64* ekeys = keys_a.as<u64>();
+
+        // 3. degrees + P1 relabel
+        DevBuf deg_old, okeys_a, okeys_b, new_id;
+        deg_old.alloc((n + 1) * sizeof(u32));
+        GL_CUDA(cudaMemsetAsync(deg_old.p, 0, (n + 1) * sizeof(u32), s));
+        if (m) {
+            k_degree<<<grid_for(m), kThreads, 0, s>>>(ekeys, m, deg_old.as<u32>());
+            GL_LAUNCH_CHECK();
+        }
+        g->b_deg.alloc((n + 1) * sizeof(u32));
+        g->b_label.alloc((n + 1) * sizeof(u64));
+        new_id.alloc((n + 1) * sizeof(u32));
+        u32 dmax = 0;
+        if (n) {
+            GL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u64), s));
+            k_dmax<<<grid_for(n), kThreads, 0, s>>>(deg_old.as<u32>(), n, (unsigned*)cnt);
+            GL_LAUNCH_CHECK();
+            GL_CUDA(cudaMemcpyAsync(&dmax, cnt, sizeof(u32), cudaMemcpyDeviceToHost, s));
+            GL_CUDA(cudaStreamSynchronize(s));
+            okeys_a.alloc(n * sizeof(u64));
+            okeys_b.alloc(n * sizeof(u64));
+            k_order_keys<<<grid_for(n), kThreads, 0, s>>>(deg_old.as<u32>(), n, okeys_a.as<u64>());
+            GL_LAUNCH_CHECK();
+            sort_keys<u64>(tmp, okeys_a.as<u64>(), okeys_b.as<u64>(), n, 32 + bits_for(dmax), s);
+            k_relabel<<<grid_for(n), kThreads, 0, s>>>(okeys_b.as<u64>(), n, labels, new_id.as<u32>(),
+                                                       g->b_deg.as<u32>(), g->b_label.as<u64>());
+            GL_LAUNCH_CHECK();
+        }
+        okeys_a.reset();
+        okeys_b.reset();
+        deg_old.reset();
+
+        // 4. id-sorted symmetric rows
+        const u64 len = 2 * m;
+        g->b_off.alloc((n + 1) * sizeof(u64));
+        GL_CUDA(cudaMemsetAsync(g->b_off.p, 0, (n + 1) * sizeof(u64), s));
+        g->b_adj.alloc((len + 1) * sizeof(u32));
+        g->b_eid.alloc((len + 1) * sizeof(u32));
+        DevBuf dir_a, dir_b, tmp64;
+        tmp64.alloc((n + 1) * sizeof(u64));
+        if (n) {
+            k_widen<<<grid_for(n), kThreads, 0, s>>>(g->b_deg.as<u32>(), n, tmp64.as<u64>());
+            GL_LAUNCH_CHECK();
+            GL_CUDA(cudaMemsetAsync(tmp64.as<u64>() + n, 0, sizeof(u64), s));
+            exclusive_scan<u64>(tmp, tmp64.as<u64>(), g->b_off.as<u64>(), n + 1, s);
+        }
+        if (m) {
+            dir_a.alloc(len * sizeof(u64));
+            dir_b.alloc(len * sizeof(u64));
+            k_directed<<<grid_for(m), kThreads, 0, s>>>(ekeys, m, new_id.as<u32>(), dir_a.as<u64>());
+            GL_LAUNCH_CHECK();
+            keys_a.reset();
+            sort_keys<u64>(tmp, dir_a.as<u64>(), dir_b.as<u64>(), len, 32 + vb, s);
+            dir_a.reset();
+            k_adj_from_dir<<<grid_for(len), kThreads, 0, s>>>(dir_b.as<u64>(), len, g->b_adj.as<u32>());
+            GL_LAUNCH_CHECK();
+        }
+        new_id.reset();
+        keys_a.reset();
+
+        // 5. oriented edge ids
+        g->b_lcnt.alloc((n + 1) * sizeof(u32));
+        g->b_loff.alloc((n + 1) * sizeof(u64));
+        GL_CUDA(cudaMemsetAsync(g->b_loff.p, 0, (n + 1) * sizeof(u64), s));
+        g->b_ev.alloc((m + 1) * sizeof(u32));
+        g->b_eu.alloc((m + 1) * sizeof(u32));
+        g->b_epos.alloc((m + 1) * sizeof(u32));
+        if (n) {
+            k_lcnt<<<grid_for(n), kThreads, 0, s>>>(g->b_off.as<u64>(), g->b_adj.as<u32>(), n,
+                                                    g->b_lcnt.as<u32>(), tmp64.as<u64>());
+            GL_LAUNCH_CHECK();
+            GL_CUDA(cudaMemsetAsync(tmp64.as<u64>() + n, 0, sizeof(u64), s));
+            exclusive_scan<u64>(tmp, tmp64.as<u64>(), g->b_loff.as<u64>(), n + 1, s);
+        }
+        if (m) {
+            k_slots<<<grid_for(len), kThreads, 0, s>>>(dir_b.as<u64>(), len, g->b_off.as<u64>(),
+                                                       g->b_adj.as<u32>(), g->b_lcnt.as<u32>(),
+                                                       g->b_loff.as<u64>(), g->b_eid.as<u32>(),
+                                                       g->b_ev.as<u32>(), g->b_eu.as<u32>(),
+                                                       g->b_epos.as<u32>());
+            GL_LAUNCH_CHECK();
+        }
+        GL_CUDA(cudaStreamSynchronize(s));
+
+        DevGraph& d = g->d;
+        d.n = n;
+        d.m = m;
+        d.dmax = dmax;
+        d.off = g->b_off.as<u64>();
+        d.adj = g->b_adj.as<u32>();
+        d.eid = g->b_eid.as<u32>();
+        d.lcnt = g->b_lcnt.as<u32>();
+        d.loff = g->b_loff.as<u64>();
+        d.ev = g->b_ev.as<u32>();
+        d.eu = g->b_eu.as<u32>();
+        d.epos = g->b_epos.as<u32>();
+        d.deg = g->b_deg.as<u32>();
+        d.label = g->b_label.as<u64>();
+        return g;
+    } catch (...) {
+        delete g;
+        throw;
+    }
+}
+
+// ------------------------------------------------------------ generators
+
+namespace {
+__global__ void k_rmat(RmatParams p, u64 count, u64* __restrict__ out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
+        u64 a, b;
+        rmat_edge(p, i, a, b);
+        out[2 * i] = a;
+        out[2 * i + 1] = b;
+    }
+}
+} // namespace
+
+void generate_rmat_device(const RmatParams& p, u64 count, u64* d_pairs, cudaStream_t s) {
+    if (count == 0) return;
+    k_rmat<<<grid_for(count), kThreads, 0, s>>>(p, count, d_pairs);
+    GL_LAUNCH_CHECK();
+}
+
+} // namespace gl

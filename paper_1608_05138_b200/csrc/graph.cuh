@@ -1,0 +1,103 @@
+// graph.cuh -- device-resident preprocessed graph (the B200 counterpart of
+// graphlet::Graph, /root/reference/proj/include/graphlet/graph.hpp:41-93).
+//
+// HBM layout (one replica per GPU):
+//   off   u64[n+1]  row offsets of the symmetric CSR
+//   adj   u32[2m]   neighbours, ascending internal id per row (P1-relabelled)
+//   eid   u32[2m]   oriented edge id of every adjacency slot
+//   lcnt  u32[n]    |L(v)| = # neighbours with smaller id; L(v) is the row
+//                   prefix, U(v) the suffix (degree-ordered DAG)
+//   loff  u64[n+1]  exclusive prefix of lcnt = first edge id with v as the
+//                   high endpoint (orient_edges order, graph.cpp:180-193)
+//   ev/eu u32[m]    endpoints of edge id e (v high, u low)
+//   epos  u32[m]    position of v inside u's row (so U(u) after v starts at
+//                   off[u] + epos + 1, and |{c in N(u) : c < v}| = epos)
+//   deg   u32[n], label u64[n]
+#pragma once
+
+#include "common.cuh"
+
+namespace gl {
+
+struct DevGraph {
+    u64 n = 0, m = 0;
+    u32 dmax = 0;
+    u64* off = nullptr;
+    u32* adj = nullptr;
+    u32* eid = nullptr;
+    u32* lcnt = nullptr;
+    u64* loff = nullptr;
+    u32* ev = nullptr;
+    u32* eu = nullptr;
+    u32* epos = nullptr;
+    u32* deg = nullptr;
+    u64* label = nullptr;
+};
+
+// RAII device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void alloc(size_t b) {
+        if (b <= bytes && p) return;
+        reset();
+        if (b == 0) b = 16;
+        GL_CUDA(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Per-graph counting state (device arrays reused across calls).
+struct CountState {
+    DevBuf t;        // u32[m]   triangles per edge
+    DevBuf tplus;    // u32[m]   triangles with this edge as the lowest pair
+    DevBuf x7, x10;  // u64[m]   micro outputs of the last shard
+    DevBuf part;     // i64[2m]  partials for the single-process path
+    DevBuf pre1;     // u64[m+1] probe prefix for the triangle kernels
+    DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
+    DevBuf items2, items3s, items3b; // work lists
+    DevBuf keys, tmp, scratch, cursor, acc; // sort keys, cub temp, kernel scratch
+    u64 n_items2 = 0, n_items3s = 0, n_items3b = 0;
+    u64 shard_begin = 0, shard_end = 0;
+    bool have_micro = false;
+    bool began = false;
+    float ms[5] = {0, 0, 0, 0, 0};
+    u32 launches = 0;
+    u64 work[4] = {0, 0, 0, 0};
+};
+
+struct Graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevGraph d;
+    DevBuf b_off, b_adj, b_eid, b_lcnt, b_loff, b_ev, b_eu, b_epos, b_deg, b_label;
+    CountState cs;
+    ~Graph() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+// build.cu
+Graph* build_graph_device(const u64* d_pairs, u64 count, int device);
+void generate_rmat_device(const RmatParams& p, u64 count, u64* d_pairs, cudaStream_t s);
+
+// count.cu
+void count_begin(Graph& g, int rank, int world, i64* d_partials, cudaStream_t s);
+void count_finish(Graph& g, const i64* d_partials, u64 begin, u64 end, u128 C[17],
+                  cudaStream_t s);
+void micro_records(const Graph& g, u64 first, u64 count, u64* host_out /* count*10 */);
+
+// algebra.cpp
+void global_from_unrestricted(const u128 C[17], u64 n, u64 m, u128 X[18]);
+
+} // namespace gl

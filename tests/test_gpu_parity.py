@@ -1,0 +1,223 @@
+"""GPU parity: the sm_100a pipeline vs the oracle / reference goldens, through the C-ABI.
+
+Bit-exact is the bar everywhere: global X_1..X_17 (128-bit) and every
+per-edge MicroRecord field (counts.cpp:122-136).
+"""
+import hashlib
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+gl = pytest.importorskip("paper_1608_05138_b200")
+from oracle import Oracle  # noqa: E402  (test infrastructure)
+
+THREADS = max(1, min(32, os.cpu_count() or 1))
+
+
+def gpu_count(pairs, device=0):
+    g = gl.Graph.build(np.asarray(pairs, dtype=np.uint64).reshape(-1, 2), device)
+    res = g.count()
+    rec = g.micro_records() if g.num_edges() else np.zeros(0, gl.MICRO_DTYPE)
+    return g, res, rec
+
+
+def assert_partitions(X, n):
+    assert X[1] + X[2] == math.comb(n, 2)
+    assert sum(X[3:7]) == math.comb(n, 3)
+    assert sum(X[7:18]) == math.comb(n, 4)
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_golden(cuda_device, name):
+    d = load_golden(name)
+    g, res, rec = gpu_count(d["pairs"], cuda_device)
+    assert g.num_vertices() == d["n"] and g.num_edges() == d["m"]
+    assert [str(x) for x in res.X] == d["X"]
+    assert hashlib.sha256(np.ascontiguousarray(rec).tobytes()).hexdigest() == d["micro_sha256"]
+    if "micro" in d:
+        assert rec.tolist() == [tuple(r) for r in d["micro"]]
+    v, u = g.orient_edges()
+    lab = g.labels()
+    got = hashlib.sha256(lab[v].astype(np.uint64).tobytes() + lab[u].astype(np.uint64).tobytes()).hexdigest()
+    assert got == d["edge_labels_sha256"]
+    assert_partitions(res.X, d["n"])
+
+
+def _er(n, p, seed):
+    rng = np.random.default_rng(seed)
+    iu = np.triu_indices(n, 1)
+    mask = rng.random(len(iu[0])) < p
+    return np.stack([iu[0][mask], iu[1][mask]], 1).astype(np.uint64)
+
+
+def test_random_corpus_vs_oracle(cuda_device):
+    """ER n in [5,60], p in {.1,.3,.5,.8,.95} and BA graphs: X and micro exact."""
+    rng = np.random.default_rng(2024)
+    for k in range(120):
+        if k % 3 == 2:
+            pairs = gl.generate_ba(int(rng.integers(5, 200)), int(rng.integers(1, 8)), seed=k)
+        else:
+            pairs = _er(int(rng.integers(5, 61)), [0.1, 0.3, 0.5, 0.8, 0.95][k % 5], k)
+        o = Oracle(pairs)
+        X, orec = o.count(micro=True)
+        g, res, rec = gpu_count(pairs, cuda_device)
+        assert res.X == X, k
+        assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE)), k
+        if o.n <= 25:
+            assert res.X == o.brute_force()
+
+
+@pytest.mark.parametrize("scale,ef", [(8, 16), (10, 8), (12, 16), (13, 16)])
+def test_rmat_vs_oracle(cuda_device, scale, ef):
+    pairs = gl.generate_rmat(scale, ef, seed=scale)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+    assert_partitions(res.X, o.n)
+
+
+@pytest.mark.parametrize("n,k", [(5000, 5), (20000, 10)])
+def test_ba_vs_oracle(cuda_device, n, k):
+    pairs = gl.generate_ba(n, k, seed=1)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
+def test_gnm_config0_vs_oracle(cuda_device):
+    """BASELINE configs[0]: G(n=10k, m=100k)."""
+    pairs = gl.generate_gnm(10000, 100000, seed=1)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert g.num_edges() == 100000
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
+def test_edge_cases(cuda_device):
+    # empty input
+    g, res, rec = gpu_count(np.zeros((0, 2), np.uint64), cuda_device)
+    assert g.num_vertices() == 0 and res.X == [0] * 18
+    # only self loops: 3 isolated vertices
+    g, res, rec = gpu_count([(5, 5), (6, 6), (7, 7), (7, 7)], cuda_device)
+    assert g.num_vertices() == 3 and g.num_edges() == 0
+    assert res.X[2] == 3 and res.X[6] == 1 and sum(res.X) == 4
+    # empty graph on n=5 (SPEC oracle example): X2=10, X6=10, X17=5
+    g, res, rec = gpu_count([(i, i) for i in range(5)], cuda_device)
+    assert res.X[2] == 10 and res.X[6] == 10 and res.X[17] == 5
+    # duplicates in both directions + label gaps + max label
+    pairs = [(2**64 - 1, 0), (0, 2**64 - 1), (3, 3), (10**15, 0), (0, 10**15), (10**15, 2**64 - 1)]
+    o = Oracle(pairs)
+    X, orec = o.count(micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X and np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+    assert sorted(g.labels().tolist()) == sorted({0, 3, 10**15, 2**64 - 1})
+
+
+@pytest.mark.parametrize("n", [5, 12, 40, 600])
+def test_complete_graphs_closed_form(cuda_device, n):
+    """K_n: X3=C(n,3), X7=C(n,4); per edge t=n-2, x7=C(n-2,2), x10=0.
+    K_600 drives T+ = 598 > the 512-entry shared-memory stage (global path)."""
+    pairs = [(a, b) for a in range(n) for b in range(a + 1, n)]
+    g, res, rec = gpu_count(pairs, cuda_device)
+    X = res.X
+    assert X[1] == math.comb(n, 2) and X[3] == math.comb(n, 3) and X[7] == math.comb(n, 4)
+    assert all(X[i] == 0 for i in (2, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17))
+    assert (rec["t"] == n - 2).all() and (rec["x7"] == math.comb(n - 2, 2)).all() and (rec["x10"] == 0).all()
+
+
+def test_cycles_and_stars_closed_form(cuda_device):
+    for n in (5, 9, 100):
+        g, res, rec = gpu_count([(i, (i + 1) % n) for i in range(n)], cuda_device)
+        assert res.X[10] == 0 and res.X[3] == 0
+    g, res, rec = gpu_count([(0, 1), (1, 2), (2, 3), (3, 0)], cuda_device)
+    assert res.X[10] == 1 and (rec["x10"] == 1).all()
+    for n in (3, 10, 3000):
+        g, res, rec = gpu_count([(0, i) for i in range(1, n + 1)], cuda_device)
+        assert res.X[11] == math.comb(n, 3) and res.X[4] == math.comb(n, 2)
+
+
+def test_big_top_windows(cuda_device):
+    """Hubs with > 512 wedges and ids > 32768 exercise k_cycle_big's multi-window path."""
+    pairs = gl.generate_ba(60000, 6, seed=3)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
+def test_sharded_equals_single(cuda_device):
+    """world=2 sharding emulated on one GPU: begin per rank, sum partial rows,
+    finish per shard, sum unrestricted -> identical macro and micro."""
+    import torch
+    pairs = gl.generate_rmat(12, 16, seed=5)
+    g = gl.Graph.build(pairs, cuda_device)
+    full = g.count()
+    full_rec = g.micro_records()
+    world = 2
+    plen = g.partials_len(world)
+    parts = []
+    for rank in range(world):
+        buf = torch.empty(2 * plen, dtype=torch.int64, device="cuda")
+        g.count_begin(rank, world, buf.data_ptr())
+        parts.append(buf)
+    total = parts[0] + parts[1]
+    torch.cuda.synchronize()
+    from paper_1608_05138_b200.dist import shard_range
+    Csum = [0] * 17
+    recs = []
+    for rank in range(world):
+        b, e = shard_range(g.num_edges(), world, rank)
+        shard = total[2 * b:2 * e].contiguous()
+        Cr = g.count_finish(shard.data_ptr(), b, e)
+        Csum = [x + y for x, y in zip(Csum, Cr)]
+        recs.append(g.micro_records(b, e - b))
+    assert gl.global_from_unrestricted(Csum, g.num_vertices(), g.num_edges()) == full.X
+    assert Csum == full.C
+    assert np.array_equal(np.concatenate(recs), full_rec)
+
+
+def test_device_generated_graph_matches_host(cuda_device):
+    import torch
+    scale, ef = 11, 16
+    host = gl.generate_rmat(scale, ef, seed=9)
+    d = torch.empty(2 * (ef << scale), dtype=torch.int64, device="cuda")
+    gl.generate_rmat_device(scale, ef, d.data_ptr(), cuda_device, seed=9)
+    assert np.array_equal(d.cpu().numpy().view(np.uint64).reshape(-1, 2), host)
+    g1 = gl.Graph.build_device(d.data_ptr(), ef << scale, cuda_device)
+    g2 = gl.Graph.build(host, cuda_device)
+    assert g1.count().X == g2.count().X
+
+
+@pytest.mark.slow
+def test_rmat20_properties_and_sample(cuda_device):
+    """BASELINE configs[1] at full size: size-independent properties plus a
+    sampled per-edge comparison with the oracle's hash pipeline."""
+    pairs = gl.generate_rmat(20, 16, seed=1)
+    g = gl.Graph.build(pairs, cuda_device)
+    res = g.count()
+    n, m = g.num_vertices(), g.num_edges()
+    assert_partitions(res.X, n)
+    t, x7, x10 = g.edge_counts()
+    assert int(t.astype(np.uint64).sum()) == 3 * res.X[3]
+    assert int(x7.sum()) == 6 * res.X[7]
+    assert int(x10.sum()) == 4 * res.X[10]
+    o = Oracle(pairs)
+    rng = np.random.default_rng(0)
+    ids = np.sort(rng.choice(m, size=300, replace=False)).astype(np.uint64)
+    ref = o.edges_hash(ids)
+    assert np.array_equal(ref[:, 0], t[ids].astype(np.uint64))
+    assert np.array_equal(ref[:, 3], x7[ids])
+    assert np.array_equal(ref[:, 4], x10[ids])

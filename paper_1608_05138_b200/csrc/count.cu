@@ -315,7 +315,6 @@ k_clique(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long l
         }
         __syncwarp();
     }
-    my_work = warp_sum_u64(my_work);
     if (lane == 0 && my_work) atomicAdd(work, (unsigned long long)my_work);
 }
 

@@ -184,7 +184,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1608_05138_b200 as gl
-    from paper_1608_05138_b200.dist import allreduce_u128, exchange_partials, shard_range
+    from paper_1608_05138_b200.dist import shard_range, sharded_step
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -216,12 +216,7 @@ def run_ours(args):
     b, e = shard_range(m, world, rank)
 
     def step():
-        g.count_begin(rank, world, partials.data_ptr(), stream.cuda_stream)
-        with torch.cuda.stream(stream):
-            shard = exchange_partials(partials, world)
-            C = g.count_finish(shard.data_ptr(), b, e, stream.cuda_stream)
-            Ct = allreduce_u128(C, device=dev) if world > 1 else C
-        return gl.global_from_unrestricted(Ct, n, m)
+        return sharded_step(g, partials, rank, world, stream)[0]
 
     for _ in range(args.warmup):
         X = step()
@@ -259,7 +254,7 @@ def run_ours(args):
     ms, nl, work = g.last_stats()
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / event time)
-    names = ["triangles", "cliques", "cycles", "epilogue"]
+    names = ["cliques_triangles", "triangle_sums", "cycles", "epilogue"]
     bytes_alg = [float(w) for w in work]  # algorithmic bytes per phase
     dom = int(np.argmax(phase_ms[:4]))
     peaks = {}
@@ -294,17 +289,12 @@ def run_ours(args):
             g2 = gl.Graph.build_host_ptr(pin_in.data_ptr(), count, local)  # gl_graph_build
             m2 = g2.num_edges()
             p2 = torch.empty(2 * g2.partials_len(world), dtype=torch.int64, device=dev)
-            g2.count_begin(rank, world, p2.data_ptr(), stream.cuda_stream)
-            with torch.cuda.stream(stream):
-                sh2 = exchange_partials(p2, world)
-                C2 = g2.count_finish(sh2.data_ptr(), b, e, stream.cuda_stream)
-                C2t = allreduce_u128(C2, device=dev) if world > 1 else C2
-            X2 = gl.global_from_unrestricted(C2t, g2.num_vertices(), m2)
+            X2, _ = sharded_step(g2, p2, rank, world, stream)
             g2.edge_counts(b, shard_n, pin_t.numpy().view(np.uint32)[:shard_n],
                            pin_x7.numpy().view(np.uint64)[:shard_n], pin_x10.numpy().view(np.uint64)[:shard_n])
             dt = (time.perf_counter() - t0) * 1e3
             g2.close()
-            del p2, sh2
+            del p2
             if i > 0:  # first iteration is warm-up
                 e2e_ms.append(dt)
             assert X2 == X, "e2e counts differ from device-resident counts"

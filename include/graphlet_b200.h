@@ -4,7 +4,7 @@
  * types cross this boundary (streams are passed as void*).
  *
  * Each entry point names the reference interface it replaces
- * (/root/reference/proj/include/graphlet/*.hpp); see INTEGRATION.md for the
+ * (/root/reference/proj/include/graphlet/ headers); see INTEGRATION.md for the
  * binding a maintainer of the reference would add.
  *
  * Error behaviour mirrors the reference's exception classes: every function
@@ -119,21 +119,28 @@ int gl_orient_edges(const gl_graph *g, uint32_t *v, uint32_t *u);
  * gl_micro_* below. */
 int gl_count(gl_graph *g, gl_graphlet_vector *X, gl_unrestricted *unres);
 
-/* Sharded form for one process per GPU:
- *  1. gl_count_begin: every rank computes the full per-edge triangle counts,
- *     then its cost-balanced share (rank of world) of the clique and cycle
- *     work, leaving per-edge int64 partials in `d_partials` (device memory of
- *     2*gl_partials_len(g, world) int64, zeroed by the callee).
- *  2. caller sums d_partials across ranks (reduce-scatter or all-reduce,
- *     e.g. NCCL), so that rank r holds the summed rows of edges
- *     [edge_begin, edge_end) at d_partials[2*edge_begin ...].
- *  3. gl_count_finish: per-edge epilogue for that shard, micro records on
- *     device, unrestricted partial sums returned in *unres.
- *  4. caller sums unres across ranks (e.g. as 32-bit limbs in int64) and
+/* Sharded form for one process per GPU.  The
+ * graph is replicated; every rank calls, in order:
+ *  1. gl_count_begin: this rank's cost-balanced share (rank of world) of the
+ *     clique/triangle pass and of the cycle pass.  Leaves per-edge int64
+ *     partial rows {x7, C4 - S} in `d_partials` (device memory of
+ *     2*gl_partials_len(g, world) int64, zeroed by the callee) and partial
+ *     per-edge triangle counts (gl_triangle_counts_device).
+ *  2. caller sums the uint32 triangle counts across ranks in place
+ *     (all-reduce; skip when world == 1).
+ *  3. gl_count_mid: this rank's share of the triangle sums S (needs all of t).
+ *  4. caller sums d_partials across ranks so that rank r holds the summed
+ *     rows of its edge shard [edge_begin, edge_end) (reduce-scatter).
+ *  5. gl_count_finish(d_shard = rows of edge_begin..edge_end): per-edge
+ *     epilogue for that shard, micro records on device, unrestricted
+ *     partial sums in *unres.
+ *  6. caller sums unres across ranks (e.g. as 32-bit limbs in int64) and
  *     calls gl_global_from_unrestricted. */
 uint64_t gl_partials_len(const gl_graph *g, int world);
 int gl_count_begin(gl_graph *g, int rank, int world, int64_t *d_partials, void *stream);
-int gl_count_finish(gl_graph *g, const int64_t *d_partials, uint64_t edge_begin,
+int gl_triangle_counts_device(gl_graph *g, uint32_t **d_t, uint64_t *count);
+int gl_count_mid(gl_graph *g, int64_t *d_partials, void *stream);
+int gl_count_finish(gl_graph *g, const int64_t *d_shard, uint64_t edge_begin,
                     uint64_t edge_end, gl_unrestricted *unres, void *stream);
 
 /* global_from_unrestricted (counts.cpp:86-111), host-side 128-bit algebra.
@@ -155,12 +162,11 @@ int gl_edge_counts_device(const gl_graph *g, const uint32_t **t, const uint64_t 
                           const uint64_t **x10);
 
 /* Kernel timing of the last count call (CUDA events on the launching stream),
- * milliseconds: [0] triangles, [1] cliques+triangle-sums, [2] cycles,
+ * milliseconds: [0] clique+triangle pass, [1] triangle sums, [2] cycles,
  * [3] epilogue+macro reduction, [4] total.  Launch count in *launches. */
 int gl_last_timings(const gl_graph *g, float ms[5], uint32_t *launches);
 /* Algorithmic work counters of the last count call:
- * [0] adjacency entries read by the triangle kernel, [1] by the clique
- * kernel, [2] by the cycle kernel, [3] edges finalised. */
+ * algorithmic bytes per phase, same order as gl_last_timings [0..3]. */
 int gl_last_work(const gl_graph *g, uint64_t work[4]);
 
 #ifdef __cplusplus

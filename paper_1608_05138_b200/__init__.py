@@ -112,6 +112,8 @@ _sig("gl_orient_edges", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 _sig("gl_count", C.c_int, C.c_void_p, C.POINTER(_GV), C.POINTER(_UC))
 _sig("gl_partials_len", C.c_uint64, C.c_void_p, C.c_int)
 _sig("gl_count_begin", C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p)
+_sig("gl_count_mid", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+_sig("gl_triangle_counts_device", C.c_int, C.c_void_p, C.POINTER(C.c_void_p), _u64p)
 _sig("gl_count_finish", C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
      C.POINTER(_UC), C.c_void_p)
 _sig("gl_global_from_unrestricted", C.c_int, C.POINTER(_UC), C.c_uint64, C.c_uint64, C.POINTER(_GV))
@@ -358,6 +360,14 @@ class Graph:
 
     def count_begin(self, rank: int, world: int, d_partials: int, stream: int = 0):
         _check(LIB.gl_count_begin(self._h, rank, world, C.c_void_p(d_partials), C.c_void_p(stream)))
+
+    def count_mid(self, d_partials: int, stream: int = 0):
+        _check(LIB.gl_count_mid(self._h, C.c_void_p(d_partials), C.c_void_p(stream)))
+
+    def triangle_counts_device(self):
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(LIB.gl_triangle_counts_device(self._h, C.byref(p), C.byref(n)))
+        return p.value, int(n.value)
 
     def count_finish(self, d_partials_shard: int, edge_begin: int, edge_end: int, stream: int = 0) -> list:
         uc = _UC()

@@ -263,6 +263,22 @@ int gl_count_begin(gl_graph* g, int rank, int world, int64_t* d_partials, void* 
     });
 }
 
+int gl_count_mid(gl_graph* g, int64_t* d_partials, void* stream) {
+    return guarded([&] {
+        auto& gr = G(g);
+        gl::count_mid(gr, reinterpret_cast<gl::i64*>(d_partials), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int gl_triangle_counts_device(gl_graph* g, uint32_t** d_t, uint64_t* count) {
+    return guarded([&] {
+        auto& gr = G(g);
+        if (!gr.cs.began) throw gl::state_error("gl_triangle_counts_device before gl_count_begin");
+        if (d_t) *d_t = gr.cs.t.as<uint32_t>();
+        if (count) *count = gr.d.m;
+    });
+}
+
 int gl_count_finish(gl_graph* g, const int64_t* d_partials, uint64_t edge_begin, uint64_t edge_end,
                     gl_unrestricted* unres, void* stream) {
     return guarded([&] {
@@ -283,6 +299,7 @@ int gl_count(gl_graph* g, gl_graphlet_vector* X, gl_unrestricted* unres) {
         const gl::u64 m = gr.d.m;
         gr.cs.part.alloc((2 * m + 2) * sizeof(gl::i64));
         gl::count_begin(gr, 0, 1, gr.cs.part.as<gl::i64>(), gr.stream);
+        gl::count_mid(gr, gr.cs.part.as<gl::i64>(), gr.stream);
         gl::u128 C[17], XX[18];
         gl::count_finish(gr, gr.cs.part.as<gl::i64>(), 0, m, C, gr.stream);
         gl::global_from_unrestricted(C, gr.d.n, m, XX);

@@ -39,14 +39,11 @@ namespace {
 
 constexpr int kTriThreads = 256;
 constexpr int kTriTile = 2048;       // probes per block tile
-constexpr int kCliqueWarps = 8;      // warps per clique block
-constexpr int kCliqueCap = 512;      // T+ entries per warp in shared memory
 constexpr int kCycleSmallWarps = 8;  // warps per small-top block
 constexpr int kHashSlots = 1024;     // per-warp hash slots (small tops)
 constexpr u64 kSmallWedges = 512;    // small-top threshold (<= half the slots)
 constexpr int kBigThreads = 1024;    // block per big top
 constexpr int kWindow = 32768;       // dense W window (u32) in shared memory
-constexpr int kChunk = 2048;         // b-chunk per flattened pass
 
 constexpr u32 kEmpty = 0xffffffffu;
 
@@ -130,11 +127,12 @@ __device__ __forceinline__ bool tri_probe(const DevGraph& g, const TriCtx& c, u6
     }
 }
 
-// MODE 0: t(e) and tplus(e).  MODE 1: S(e) contributions into y rows.
-template <int MODE>
+// S(e) contributions: for every triangle (u < v < c) found at its lowest pair
+// e = (v,u) by one probe of the shorter list, credit -(t of the other two
+// edges) into the y rows of all three edges (y = C4 - S).
 __global__ void __launch_bounds__(kTriThreads)
-k_tri(DevGraph g, const u64* __restrict__ pre, u64 item_begin, u64 item_end, u32* __restrict__ t,
-      u32* __restrict__ tplus, i64* __restrict__ part) {
+k_trisum(DevGraph g, const u64* __restrict__ pre, u64 item_begin, u64 item_end, const u32* __restrict__ t,
+         i64* __restrict__ part) {
     __shared__ u64 s_e[2];
     for (u64 tile = item_begin + (u64)blockIdx.x * kTriTile; tile < item_end;
          tile += (u64)gridDim.x * kTriTile) {
@@ -145,177 +143,259 @@ k_tri(DevGraph g, const u64* __restrict__ pre, u64 item_begin, u64 item_end, u32
             s_e[threadIdx.x] = upper_bound_dev<u64, u64>(pre, 0, g.m + 1, x) - 1;
         }
         __syncthreads();
-        const u64 e_lo = s_e[0], e_hi = s_e[1] + 1;
+        const u64 e_lo = s_e[0], e_end = s_e[1] + 1;
         for (u64 base = tile; base < tile_end; base += kTriThreads) {
             const u64 i = base + threadIdx.x;
             const bool valid = i < tile_end;
             u64 e = ~0ull;
-            bool found = false;
-            u64 sa = 0, sb = 0;
+            u64 contrib = 0;
             if (valid) {
-                e = upper_bound_dev<u64, u64>(pre, e_lo, e_hi + 1 > g.m + 1 ? g.m + 1 : e_hi + 1, i) - 1;
+                e = upper_bound_dev<u64, u64>(pre, e_lo, e_end, i) - 1;
                 TriCtx c = tri_ctx(g, e);
-                found = tri_probe(g, c, i - pre[e], &sa, &sb);
-            }
-            if (MODE == 0) {
-                if (found) {
-                    atomicAdd(&t[g.eid[sa]], 1u);
-                    atomicAdd(&t[g.eid[sb]], 1u);
-                }
-                u64 sum;
-                bool tail = seg_tail_sum(e, found ? 1ull : 0ull, &sum);
-                if (valid && tail && sum) {
-                    atomicAdd(&t[e], (u32)sum);
-                    atomicAdd(&tplus[e], (u32)sum);
-                }
-            } else {
-                u64 contrib = 0;
-                if (found) {
+                u64 sa = 0, sb = 0;
+                if (tri_probe(g, c, i - pre[e], &sa, &sb)) {
                     u32 ea = g.eid[sa], eb = g.eid[sb];
                     u64 te = t[e], ta = t[ea], tb = t[eb];
                     atomic_add_i64(&part[2 * (u64)ea + 1], -(i64)(te + tb));
                     atomic_add_i64(&part[2 * (u64)eb + 1], -(i64)(te + ta));
                     contrib = ta + tb;
                 }
-                u64 sum;
-                bool tail = seg_tail_sum(e, contrib, &sum);
-                if (valid && tail && sum) atomic_add_i64(&part[2 * e + 1], -(i64)sum);
             }
+            u64 sum;
+            bool tail = seg_tail_sum(e, contrib, &sum);
+            if (valid && tail && sum) atomic_add_i64(&part[2 * e + 1], -(i64)sum);
         }
     }
 }
 
 // ------------------------------------------------------------------ cliques
+//
+// Per lowest vertex a, the out-neighbourhood H_a = G[U(a)] is staged as a
+// bitmap adjacency matrix (ceil(k/32) u32 words per row, k = |U(a)|).  Every
+// triangle (a < x < y) is an edge (x,y) of H_a and every 4-clique
+// (a < x < y < z) a triangle of H_a, so one pass over all a yields, each
+// exactly once:
+//   t(x,y)  += 1                       t(a,x)  += deg_H(x)
+//   x7(x,y) += |N_H(x) n N_H(y)|       x7(a,x) += #triangles of H_a at x
+// Global atomics are per triangle, never per 4-clique (a 4-clique is only
+// ever a popcount of an AND of two shared-memory rows).
 
-// Warp-local T+ staging: c, deg (clique degree inside T+), eid(u,c), eid(v,c),
-// flattened work prefix.
-struct TBuf {
-    u32 *c, *deg, *eu, *ev, *pre;
-};
+constexpr int kHWarpMax = 32;       // 2 <= k <= 32: one warp, one u32 row per lane
+constexpr int kHWarpsPerBlock = 8;
+constexpr int kHBlockThreads = 512; // k > 32: one block per vertex
+constexpr int kHSmemMax = 768;      // k <= 768: workspace in shared memory
 
-__device__ __forceinline__ TBuf tbuf_at(u32* base, u32 cap) {
-    TBuf b;
-    b.c = base;
-    b.deg = base + cap;
-    b.eu = base + 2 * cap;
-    b.ev = base + 3 * cap;
-    b.pre = base + 4 * cap;
-    return b;
+__device__ __forceinline__ u64 u_begin(const DevGraph& g, u32 x) { return g.off[x] + g.lcnt[x]; }
+
+__global__ void __launch_bounds__(kHWarpsPerBlock * 32)
+k_hclique_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
+               u32* __restrict__ t, i64* __restrict__ part) {
+    __shared__ u32 s_x[kHWarpsPerBlock][32];
+    __shared__ u32 s_row[kHWarpsPerBlock][32];
+    const u32 lane = lane_id(), wib = threadIdx.x >> 5;
+    u32* xs = s_x[wib];
+    u32* rows = s_row[wib];
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(queue, 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= n_items) break;
+        const u32 a = items[idx];
+        const u64 ub = u_begin(g, a);
+        const u32 k = (u32)(g.off[a + 1] - ub);
+        u32 x = 0;
+        u64 xb = 0, xe = 0;
+        if (lane < k) {
+            x = g.adj[ub + lane];
+            xb = u_begin(g, x);
+            xe = g.off[x + 1];
+        }
+        xs[lane] = x;
+        __syncwarp();
+        // phase 1: upper row, bit j > lane set iff x_j in U(x)
+        u32 row = 0;
+        if (lane + 1 < k) {
+            const u32 rem = k - 1 - lane;
+            if (xe - xb <= rem) {
+                for (u64 p = xb; p < xe; ++p) {
+                    u32 y = g.adj[p];
+                    u32 j = lower_bound_dev<u32, u32>(xs, lane + 1, k, y);
+                    if (j < k && xs[j] == y) row |= 1u << j;
+                }
+            } else {
+                for (u32 j = lane + 1; j < k; ++j) {
+                    u32 y = xs[j];
+                    u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
+                    if (p < xe && g.adj[p] == y) row |= 1u << j;
+                }
+            }
+        }
+        // symmetrise: lane j collects the lanes whose upper row names j
+        u32 col = 0;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            u32 b = __ballot_sync(0xffffffffu, (row >> j) & 1u);
+            if (lane == (u32)j) col = b;
+        }
+        const u32 full = row | col;
+        rows[lane] = full;
+        __syncwarp();
+        // phase 2: per H-edge common neighbours
+        u32 tri = 0;
+        u32 bits = full;
+        while (bits) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const u32 c = __popc(full & rows[j]);
+            tri += c;
+            if ((u32)j > lane) {
+                const u32 y = xs[j];
+                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
+                const u32 e = g.eid[p];
+                atomicAdd(&t[e], 1u);
+                if (c) atomic_add_i64(&part[2 * (u64)e], (i64)c);
+            }
+        }
+        if (lane < k) {
+            const u32 deg = __popc(full);
+            const u32 e = g.eid[ub + lane];
+            if (deg) atomicAdd(&t[e], deg);
+            if (tri) atomic_add_i64(&part[2 * (u64)e], (i64)(tri >> 1));
+        }
+        __syncwarp();
+    }
+}
+
+// In-place exclusive scan of n u32 (generic pointer) by the whole block;
+// returns the total.  Chunks of 2*blockDim with a running carry.
+template <int THREADS>
+__device__ u32 block_exclusive_scan(u32* a, u32 n) {
+    using BlockScan = cub::BlockScan<u32, THREADS>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ u32 s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (u32 base = 0; base < n; base += 2 * THREADS) {
+        u32 v[2];
+        const u32 i0 = base + 2 * threadIdx.x;
+        v[0] = i0 < n ? a[i0] : 0;
+        v[1] = i0 + 1 < n ? a[i0 + 1] : 0;
+        u32 total;
+        BlockScan(tmp).ExclusiveSum(v, v, total);
+        const u32 carry = s_carry;
+        if (i0 < n) a[i0] = v[0] + carry;
+        if (i0 + 1 < n) a[i0 + 1] = v[1] + carry;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    return s_carry;
+}
+
+__device__ __forceinline__ u64 hblock_ws_words(u32 k) {
+    return 3ull * k + 1 + (u64)k * ((k + 31) >> 5);
+}
+
+__global__ void __launch_bounds__(kHBlockThreads)
+k_hclique_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
+                u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride) {
+    extern __shared__ u32 smem[];
+    __shared__ unsigned long long s_idx;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
+        __syncthreads();
+        const unsigned long long idx = s_idx;
+        if (idx >= n_items) break;
+        const u32 a = items[idx];
+        const u64 ub = u_begin(g, a);
+        const u32 k = (u32)(g.off[a + 1] - ub);
+        const u32 W = (k + 31) >> 5;
+        u32* ws = k <= (u32)kHSmemMax ? smem : gscratch + (u64)blockIdx.x * gstride;
+        u32* xs = ws;
+        u32* pre = xs + k;
+        u32* tri = pre + k + 1;
+        u32* rows = tri + k;
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+            const u32 x = g.adj[ub + i];
+            xs[i] = x;
+            tri[i] = 0;
+            const u64 lu = g.off[x + 1] - u_begin(g, x);
+            const u32 rem = k - 1 - i;
+            pre[i] = (u32)(lu < rem ? lu : rem);
+        }
+        for (u64 w = threadIdx.x; w < (u64)k * W; w += blockDim.x) rows[w] = 0;
+        __syncthreads();
+        const u32 Q = block_exclusive_scan<kHBlockThreads>(pre, k);
+        if (threadIdx.x == 0) pre[k] = Q;
+        __syncthreads();
+        // phase 1: flattened probes set both mirror bits
+        for (u32 q = threadIdx.x; q < Q; q += blockDim.x) {
+            const u32 i = upper_bound_dev<u32, u32>(pre, 0, k + 1, q) - 1;
+            const u32 r = q - pre[i];
+            const u32 x = xs[i];
+            const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+            u32 j;
+            bool found;
+            if (xe - xb <= (u64)(k - 1 - i)) {
+                const u32 y = g.adj[xb + r];
+                j = lower_bound_dev<u32, u32>(xs, i + 1, k, y);
+                found = j < k && xs[j] == y;
+            } else {
+                j = i + 1 + r;
+                const u32 y = xs[j];
+                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
+                found = p < xe && g.adj[p] == y;
+            }
+            if (found) {
+                atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
+                atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
+            }
+        }
+        __syncthreads();
+        // phase 2: H-edges (i < j) by row word; popcount of row ANDs
+        for (u64 q = threadIdx.x; q < (u64)k * W; q += blockDim.x) {
+            const u32 i = (u32)(q / W), w = (u32)(q % W);
+            if (w < (i >> 5)) continue;
+            u32 bits = rows[q];
+            if (w == (i >> 5)) bits &= (i & 31) == 31 ? 0u : (~0u << ((i & 31) + 1));
+            if (!bits) continue;
+            const u32 x = xs[i];
+            const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+            const u32* ri = rows + (u64)i * W;
+            while (bits) {
+                const u32 j = w * 32 + (__ffs(bits) - 1);
+                bits &= bits - 1;
+                const u32* rj = rows + (u64)j * W;
+                u32 c = 0;
+                for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
+                if (c) {
+                    atomicAdd(&tri[i], c);
+                    atomicAdd(&tri[j], c);
+                }
+                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
+                const u32 e = g.eid[p];
+                atomicAdd(&t[e], 1u);
+                if (c) atomic_add_i64(&part[2 * (u64)e], (i64)c);
+            }
+        }
+        __syncthreads();
+        // phase 3: edges (a, x_i)
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+            u32 deg = 0;
+            const u32* ri = rows + (u64)i * W;
+            for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
+            const u32 e = g.eid[ub + i];
+            if (deg) atomicAdd(&t[e], deg);
+            if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
+        }
+    }
 }
 
 __device__ __forceinline__ u64 warp_sum_u64(u64 v) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     return v;
-}
-
-__global__ void __launch_bounds__(kCliqueWarps * 32)
-k_clique(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-         i64* __restrict__ part, u32* __restrict__ gscratch, u32 gcap, unsigned long long* __restrict__ work) {
-    extern __shared__ u32 smem[];
-    const u32 lane = lane_id();
-    const u32 wib = threadIdx.x >> 5;
-    const u64 gwarp = (u64)blockIdx.x * kCliqueWarps + wib;
-    u64 my_work = 0;
-    for (;;) {
-        unsigned long long idx = 0;
-        if (lane == 0) idx = atomicAdd(queue, 1ull);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= n_items) break;
-        const u64 e = items[idx];
-        TriCtx c = tri_ctx(g, e);
-        const u64 la = c.a_end - c.a_begin, lb = c.b_end - c.b_begin;
-        const u64 ls = la < lb ? la : lb;
-        const bool big = ls > (u64)kCliqueCap;
-        TBuf tb = big ? tbuf_at(gscratch + gwarp * 5ull * gcap, gcap)
-                      : tbuf_at(smem + wib * 5u * kCliqueCap, kCliqueCap);
-        // 1. T+ = U(u) after v  n  U(v), in ascending id order
-        u32 T = 0;
-        for (u64 base = 0; base < ls; base += 32) {
-            u64 r = base + lane;
-            u64 sa = 0, sb = 0;
-            bool found = r < ls && tri_probe(g, c, r, &sa, &sb);
-            unsigned bal = __ballot_sync(0xffffffffu, found);
-            if (found) {
-                u32 pos = T + __popc(bal & ((1u << lane) - 1u));
-                tb.c[pos] = g.adj[sa];
-                tb.eu[pos] = g.eid[sa];
-                tb.ev[pos] = g.eid[sb];
-                tb.deg[pos] = 0;
-            }
-            T += __popc(bal);
-        }
-        my_work += ls;
-        __syncwarp();
-        // 2. per-member work = min(|U(c)|, members after c); exclusive prefix
-        u32 carry = 0;
-        for (u32 base = 0; base < T; base += 32) {
-            u32 i = base + lane;
-            u32 w = 0;
-            if (i < T) {
-                u32 x = tb.c[i];
-                u64 lu = g.off[x + 1] - (g.off[x] + g.lcnt[x]);
-                u64 rem = T - 1 - i;
-                w = (u32)(lu < rem ? lu : rem);
-            }
-            u32 incl = w;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                u32 o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= (u32)d) incl += o;
-            }
-            if (i < T) tb.pre[i] = carry + incl - w;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        const u32 W2 = carry;
-        __syncwarp();
-        // 3. flattened intersections: edges (c, d) inside T+
-        u64 K = 0;
-        for (u32 base = 0; base < W2; base += 32) {
-            u32 k = base + lane;
-            if (k < W2) {
-                u32 i = upper_bound_dev<u32, u32>(tb.pre, 0, T, k) - 1;
-                u32 r = k - tb.pre[i];
-                u32 x = tb.c[i];
-                u64 ub = g.off[x] + g.lcnt[x], ue = g.off[x + 1];
-                u64 lu = ue - ub;
-                u32 rem = T - 1 - i;
-                bool found;
-                u32 j;
-                u64 slot;
-                if (lu <= rem) {
-                    slot = ub + r;
-                    u32 d = g.adj[slot];
-                    j = lower_bound_dev<u32, u32>(tb.c, i + 1, T, d);
-                    found = j < T && tb.c[j] == d;
-                } else {
-                    j = i + 1 + r;
-                    u32 d = tb.c[j];
-                    slot = lower_bound_dev<u32, u64>(g.adj, ub, ue, d);
-                    found = slot < ue && g.adj[slot] == d;
-                }
-                if (found) {
-                    atomicAdd(&tb.deg[i], 1u);
-                    atomicAdd(&tb.deg[j], 1u);
-                    ++K;
-                    atomic_add_i64(&part[2 * (u64)g.eid[slot]], 1); // top edge (c, d)
-                }
-            }
-        }
-        my_work += W2;
-        __syncwarp();
-        K = warp_sum_u64(K);
-        if (lane == 0 && K) atomic_add_i64(&part[2 * e], (i64)K);
-        for (u32 i = lane; i < T; i += 32) {
-            u32 d = tb.deg[i];
-            if (d) {
-                atomic_add_i64(&part[2 * (u64)tb.eu[i]], (i64)d);
-                atomic_add_i64(&part[2 * (u64)tb.ev[i]], (i64)d);
-            }
-        }
-        __syncwarp();
-    }
-    if (lane == 0 && my_work) atomicAdd(work, (unsigned long long)my_work);
 }
 
 // ------------------------------------------------------------------ cycles
@@ -326,7 +406,7 @@ static_assert(kHashSlots == 1024, "hslot assumes 1024 slots");
 // Small tops: one warp per top vertex a, W[c] in a warp-private hash.
 __global__ void __launch_bounds__(kCycleSmallWarps * 32)
 k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ items, u64 n_items,
-              unsigned long long* __restrict__ queue, i64* __restrict__ part) {
+              unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc) {
     extern __shared__ u32 smem[];
     const u32 lane = lane_id();
     const u32 wib = threadIdx.x >> 5;
@@ -377,11 +457,11 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
                 u32 h = hslot(cv);
                 while (keys[h] != cv) h = (h + 1) & (kHashSlots - 1);
                 val = cnt[h] - 1;
-                if (val) atomic_add_i64(&part[2 * (u64)g.eid[slot] + 1], (i64)val);
+                if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
             }
             u64 sum;
             bool tail = seg_tail_sum(e, val, &sum);
-            if (k < nw && tail && sum) atomic_add_i64(&part[2 * e + 1], (i64)sum);
+            if (k < nw && tail && sum) atomic_add_i64(&slot_acc[g.off[a] + (e - E0)], (i64)sum);
         }
         __syncwarp();
         for (u32 i = lane; i < kHashSlots; i += 32) {
@@ -392,38 +472,26 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
     }
 }
 
-// Block-wide exclusive scan of up to kChunk u32 values (kBigThreads threads,
-// 2 values per thread).  Returns the total.
-__device__ __forceinline__ u32 block_scan_chunk(u32* s_vals, u32 n, u32* s_warp) {
-    using BlockScan = cub::BlockScan<u32, kBigThreads>;
-    __shared__ typename BlockScan::TempStorage tmp;
-    (void)s_warp;
-    u32 v[2];
-    const u32 t = threadIdx.x;
-    v[0] = (2 * t < n) ? s_vals[2 * t] : 0;
-    v[1] = (2 * t + 1 < n) ? s_vals[2 * t + 1] : 0;
-    u32 total;
-    BlockScan(tmp).ExclusiveSum(v, v, total);
-    __syncthreads();
-    if (2 * t < n) s_vals[2 * t] = v[0];
-    if (2 * t + 1 < n) s_vals[2 * t + 1] = v[1];
-    __syncthreads();
-    return total;
-}
-static_assert(kChunk == 2 * kBigThreads, "chunk = 2 items per thread");
-
 // Big tops: one block per top vertex a, dense W windows in shared memory.
+// Work inside a window is expanded per warp tile of 32 lower neighbours b:
+// lane i owns b_i's run N(b_i) n [lo,hi) (cursor-resumed), the tile's runs
+// are prefix-summed with shuffles and every lane then walks consecutive
+// wedges, finding its owner lane by a 5-step shuffle search.  Credits go to
+// per-adjacency-slot accumulators (consecutive slots of one row are
+// consecutive addresses), folded into edge rows by k_fold_slots.
 __global__ void __launch_bounds__(kBigThreads, 1)
 k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-            i64* __restrict__ part, u32* __restrict__ gcur, u32 gcur_cap) {
-    extern __shared__ u32 smem[];
-    u32* W = smem;                    // kWindow
-    u32* s_pre = smem + kWindow;      // kChunk + 1
+            i64* __restrict__ slot_acc, u32* __restrict__ gcur, u32 gcur_cap) {
+    extern __shared__ u32 W[]; // kWindow counters
     __shared__ unsigned long long s_idx;
     __shared__ u32 s_next;
+    __shared__ unsigned long long s_total;
+    __shared__ unsigned long long s_bsum[kBigThreads / 32][32];
+    const u32 lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     u32* cur = gcur + (u64)blockIdx.x * 2 * gcur_cap;
     u32* hpos = cur + gcur_cap;
     for (u32 i = threadIdx.x; i < kWindow; i += blockDim.x) W[i] = 0;
+    s_bsum[wid][lane] = 0;
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
@@ -433,74 +501,115 @@ k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lon
         const u32 a = items[idx];
         const u64 E0 = g.loff[a];
         const u32 nb = (u32)(g.loff[a + 1] - E0);
+        const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
         if (threadIdx.x == 0) s_next = kEmpty;
         __syncthreads();
         for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
             cur[j] = 0;
-            u64 e = E0 + j;
+            const u64 e = E0 + j;
             if (g.epos[e] > 0) atomicMin(&s_next, g.adj[g.off[g.eu[e]]]);
         }
         __syncthreads();
         u32 lo = s_next;
         while (lo != kEmpty && lo < a) {
             const u32 hi = (u64)lo + kWindow < (u64)a ? lo + kWindow : a;
-            // run ends for this window
-            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
-                u64 e = E0 + j;
-                u64 rb = g.off[g.eu[e]];
-                u64 p = lower_bound_dev<u32, u64>(g.adj, rb + cur[j], rb + g.epos[e], hi);
-                hpos[j] = (u32)(p - rb);
-            }
+            if (threadIdx.x == 0) s_total = 0;
             __syncthreads();
-            // three flattened passes: count, credit, clear
-            for (int pass = 0; pass < 3; ++pass) {
-                for (u32 cb = 0; cb < nb; cb += kChunk) {
-                    const u32 cn = nb - cb < (u32)kChunk ? nb - cb : (u32)kChunk;
-                    for (u32 j = threadIdx.x; j < cn; j += blockDim.x) s_pre[j] = hpos[cb + j] - cur[cb + j];
-                    __syncthreads();
-                    const u32 total = block_scan_chunk(s_pre, cn, nullptr);
-                    if (threadIdx.x == 0) s_pre[cn] = total;
-                    __syncthreads();
-                    for (u32 base = 0; base < total; base += blockDim.x) {
-                        const u32 k = base + threadIdx.x;
-                        u64 key = ~0ull, val = 0;
+            u64 mytot = 0;
+            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
+                const u64 e = E0 + j;
+                const u64 rb = g.off[g.eu[e]];
+                const u32 c0 = cur[j];
+                const u64 p = lower_bound_dev<u32, u64>(g.adj, rb + c0, rb + g.epos[e], hi);
+                hpos[j] = (u32)(p - rb);
+                mytot += p - rb - c0;
+            }
+            mytot = warp_sum_u64(mytot);
+            if (lane == 0 && mytot) atomicAdd(&s_total, (unsigned long long)mytot);
+            __syncthreads();
+            const bool bulk_clear = s_total > (unsigned long long)(kWindow / 4);
+            for (int pass = 0; pass < (bulk_clear ? 2 : 3); ++pass) {
+                for (u32 tile = wid * 32; tile < nb; tile += nwarps * 32) {
+                    const u32 j = tile + lane;
+                    u64 rs = 0;
+                    u32 len = 0;
+                    if (j < nb) {
+                        const u64 e = E0 + j;
+                        const u32 c0 = cur[j];
+                        rs = g.off[g.eu[e]] + c0;
+                        len = hpos[j] - c0;
+                    }
+                    u32 incl = len;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+                        if (lane >= (u32)d) incl += o;
+                    }
+                    const u32 excl = incl - len;
+                    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+                    for (u32 base = 0; base < total; base += 32) {
+                        const u32 k = base + lane;
+                        u32 owner = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const u32 cand = owner + step;
+                            const u32 ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                            if (cand < 32 && ex <= k) owner = cand;
+                        }
+                        const u32 oex = __shfl_sync(0xffffffffu, excl, owner);
+                        const u64 ors = __shfl_sync(0xffffffffu, rs, owner);
                         if (k < total) {
-                            u32 jj = upper_bound_dev<u32, u32>(s_pre, 0, cn + 1, k) - 1;
-                            // skip empty runs (equal prefixes): upper_bound lands on the last equal
-                            u32 j = cb + jj;
-                            u64 e = E0 + j;
-                            u64 slot = g.off[g.eu[e]] + cur[j] + (k - s_pre[jj]);
-                            u32 cv = g.adj[slot];
+                            const u64 slot = ors + (k - oex);
+                            const u32 cv = g.adj[slot];
                             if (pass == 0) {
                                 atomicAdd(&W[cv - lo], 1u);
                             } else if (pass == 1) {
-                                val = W[cv - lo] - 1;
-                                key = e;
-                                if (val) atomic_add_i64(&part[2 * (u64)g.eid[slot] + 1], (i64)val);
+                                const u32 val = W[cv - lo] - 1;
+                                if (val) {
+                                    atomic_add_i64(&slot_acc[slot], (i64)val);
+                                    atomicAdd(&s_bsum[wid][owner], (unsigned long long)val);
+                                }
                             } else {
                                 W[cv - lo] = 0;
                             }
                         }
-                        if (pass == 1) {
-                            u64 sum;
-                            bool tail = seg_tail_sum(key, val, &sum);
-                            if (k < total && tail && sum) atomic_add_i64(&part[2 * key + 1], (i64)sum);
-                        }
                     }
-                    __syncthreads();
+                    if (pass == 1) {
+                        __syncwarp();
+                        const unsigned long long bs = s_bsum[wid][lane];
+                        if (bs) {
+                            atomic_add_i64(&slot_acc[abase + j], (i64)bs);
+                            s_bsum[wid][lane] = 0;
+                        }
+                        __syncwarp();
+                    }
                 }
+                __syncthreads();
             }
-            // advance cursors, find next non-empty window start
+            if (bulk_clear) {
+                for (u32 i = threadIdx.x; i < hi - lo; i += blockDim.x) W[i] = 0;
+            }
+            // advance cursors, next non-empty window start
             if (threadIdx.x == 0) s_next = kEmpty;
             __syncthreads();
             for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
-                cur[j] = hpos[j];
-                u64 e = E0 + j;
-                if (cur[j] < g.epos[e]) atomicMin(&s_next, g.adj[g.off[g.eu[e]] + cur[j]]);
+                const u32 h = hpos[j];
+                cur[j] = h;
+                const u64 e = E0 + j;
+                if (h < g.epos[e]) atomicMin(&s_next, g.adj[g.off[g.eu[e]] + h]);
             }
             __syncthreads();
             lo = s_next;
         }
+    }
+}
+
+// y(e) += the two adjacency-slot accumulators of edge e (v's row, u's row).
+__global__ void k_fold_slots(DevGraph g, const i64* __restrict__ slot_acc, i64* __restrict__ part) {
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < g.m; e += (u64)gridDim.x * blockDim.x) {
+        const u32 v = g.ev[e], u = g.eu[e];
+        const i64 s = slot_acc[g.off[v] + (e - g.loff[v])] + slot_acc[g.off[u] + g.epos[e]];
+        if (s) part[2 * e + 1] += s;
     }
 }
 
@@ -591,16 +700,19 @@ __global__ void k_seq(u32* __restrict__ ids, u64 n) {
         ids[i] = (u32)i;
 }
 
-__global__ void k_clique_keys(const u32* __restrict__ tplus, const u64* __restrict__ probes, u64 m,
-                              u64* __restrict__ keys, unsigned long long* __restrict__ cnt) {
-    u32 local = 0;
-    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < m; e += (u64)gridDim.x * blockDim.x) {
-        u64 tp = tplus[e];
-        u64 k = tp >= 2 ? tp * (tp + 8) + probes[e] : 0;
-        keys[e] = k;
-        local += k ? 1 : 0;
+// |U(a)| for the H-pass work list (vertices with >= 2 up-neighbours)
+__global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* __restrict__ cnt) {
+    unsigned long long lb = 0, ls = 0;
+    for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
+        u64 k = g.off[a + 1] - (g.off[a] + g.lcnt[a]);
+        keys[a] = k >= 2 ? k : 0;
+        if (k > (u64)kHWarpMax)
+            ++lb;
+        else if (k >= 2)
+            ++ls;
     }
-    if (local) atomicAdd(cnt, (unsigned long long)local);
+    if (lb) atomicAdd(&cnt[0], lb);
+    if (ls) atomicAdd(&cnt[1], ls);
 }
 
 __global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u64* __restrict__ keys,
@@ -626,24 +738,6 @@ __global__ void k_take_rank(const u32* __restrict__ sorted, u64 begin, u64 count
         if (p >= count) break;
         out[i] = sorted[begin + p];
     }
-}
-
-__global__ void k_max_u32(const u32* __restrict__ a, const u32* __restrict__ ids, u64 n,
-                          const DevGraph g, unsigned* __restrict__ out) {
-    u32 mx = 0;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        u64 e = ids[i];
-        TriCtx c = tri_ctx(g, e);
-        u64 la = c.a_end - c.a_begin, lb = c.b_end - c.b_begin;
-        u32 v = (u32)(la < lb ? la : lb);
-        mx = v > mx ? v : mx;
-    }
-    (void)a;
-    for (int d = 16; d > 0; d >>= 1) {
-        u32 o = __shfl_down_sync(0xffffffffu, mx, d);
-        mx = o > mx ? o : mx;
-    }
-    if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
 struct Timer {
@@ -687,6 +781,17 @@ template <typename T> T read_dev(const T* p, cudaStream_t s) {
 
 // --------------------------------------------------------------------------
 
+namespace {
+
+// Cost-sorted vertex work list (descending key) and this rank's share of
+// the sorted positions [begin, begin+count): p % world == rank.
+u64 rank_share(u64 count, int rank, int world) {
+    return count > (u64)rank ? (count - rank + world - 1) / world : 0;
+}
+
+} // namespace
+
+// Phase A: H-pass (t and x7 partials) and the cycle kernels (C4 into y).
 void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s) {
     GL_CUDA(cudaSetDevice(gr.device));
     if (world < 1 || rank < 0 || rank >= world) throw invalid_argument("bad rank/world");
@@ -697,10 +802,12 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     const u64 m = g.m, n = g.n;
     cs.launches = 0;
     cs.began = false;
+    cs.mid_done = false;
+    cs.rank = rank;
+    cs.world = world;
     std::memset(cs.work, 0, sizeof(cs.work));
 
     cs.t.alloc((m + 1) * sizeof(u32));
-    cs.tplus.alloc((m + 1) * sizeof(u32));
     cs.pre1.alloc((m + 1) * sizeof(u64));
     cs.wpre.alloc((m + 1) * sizeof(u64));
     cs.acc.alloc(64 * sizeof(u64));
@@ -709,16 +816,17 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     const u64 plen = ((m + world - 1) / world) * (u64)world;
     if (plen) GL_CUDA(cudaMemsetAsync(d_partials, 0, 2 * plen * sizeof(i64), s));
     GL_CUDA(cudaMemsetAsync(cs.t.p, 0, (m + 1) * sizeof(u32), s));
-    GL_CUDA(cudaMemsetAsync(cs.tplus.p, 0, (m + 1) * sizeof(u32), s));
+    cs.slots.alloc((2 * m + 1) * sizeof(i64));
+    GL_CUDA(cudaMemsetAsync(cs.slots.p, 0, (2 * m + 1) * sizeof(i64), s));
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40; // queues + counts
     GL_CUDA(cudaMemsetAsync(counters, 0, 24 * sizeof(u64), s));
 
     Timer tm(4);
     GL_CUDA(cudaEventRecord(tm.ev[0], s));
     if (m == 0) {
-        for (int i = 1; i < 4; ++i) GL_CUDA(cudaEventRecord(tm.ev[i], s));
+        for (int i = 1; i < 3; ++i) GL_CUDA(cudaEventRecord(tm.ev[i], s));
     } else {
-        u64* probes = cs.keys.as<u64>();     // scratch reuse before the sorts
+        u64* probes = cs.keys.as<u64>(); // scratch reuse before the sorts
         u64* wedges = probes + (m + 1);
         k_prepass<<<grid1d(m, 256, sms), 256, 0, s>>>(g, probes, wedges, counters + 17);
         GL_LAUNCH_CHECK();
@@ -726,68 +834,58 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
         GL_CUDA(cudaMemsetAsync(wedges + m, 0, sizeof(u64), s));
         dev_exclusive_scan<u64>(cs.tmp, probes, cs.pre1.as<u64>(), m + 1, s);
         dev_exclusive_scan<u64>(cs.tmp, wedges, cs.wpre.as<u64>(), m + 1, s);
-        cs.launches += 3;
-        const u64 P = read_dev(cs.pre1.as<u64>() + m, s);
-        const u64 L = read_dev<unsigned long long>(counters + 17, s);
-        cs.work[0] = 4 * L; // t pass; the S pass adds this rank's slice below
+        cs.launches += 5;
+        cs.probes = read_dev(cs.pre1.as<u64>() + m, s);
+        cs.lsum = read_dev<unsigned long long>(counters + 17, s);
+        cs.work[0] = 4 * cs.lsum / (u64)world; // H-pass builds every H_a row by intersection
 
-        // triangles (replicated on every rank: every rank needs all of t)
-        if (P) {
-            unsigned gt = (unsigned)std::min<u64>((P + kTriTile - 1) / kTriTile, (u64)sms * 8);
-            k_tri<0><<<gt, kTriThreads, 0, s>>>(g, cs.pre1.as<u64>(), 0, P, cs.t.as<u32>(),
-                                                  cs.tplus.as<u32>(), d_partials);
-            GL_LAUNCH_CHECK();
-            // triangle sums S, this rank's slice of the probe space
-            u64 b = P * (u64)rank / world, en = P * (u64)(rank + 1) / world;
-            if (en > b) {
-                unsigned gs = (unsigned)std::min<u64>((en - b + kTriTile - 1) / kTriTile, (u64)sms * 8);
-                k_tri<1><<<gs, kTriThreads, 0, s>>>(g, cs.pre1.as<u64>(), b, en, cs.t.as<u32>(),
-                                                      cs.tplus.as<u32>(), d_partials);
-                GL_LAUNCH_CHECK();
-                cs.work[0] += (u64)((double)(4 * L) * (double)(en - b) / (double)P);
-            }
-            cs.launches += 2;
-        }
-        GL_CUDA(cudaEventRecord(tm.ev[1], s));
-
-        // cliques: lowest pairs with |T+| >= 2, cost-sorted, rank share
+        // H-pass: vertices by |U(a)| descending; k > 32 block kernel, else warp kernel
         {
             u64* kin = cs.keys.as<u64>();
-            u64* kout = kin + (m + 1);
+            u64* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
-            u32* iout = iin + (m + 1);
-            // probes still needed for the key: recompute into kout first
-            k_prepass<<<grid1d(m, 256, sms), 256, 0, s>>>(g, kout, kin, nullptr); // kout=probes, kin=wedges(unused)
-            k_clique_keys<<<grid1d(m, 256, sms), 256, 0, s>>>(cs.tplus.as<u32>(), kout, m, kin, counters + 8);
-            k_seq<<<grid1d(m, 256, sms), 256, 0, s>>>(iin, m);
+            u32* iout = iin + (n + 1);
+            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12);
+            k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
-            dev_sort_desc(cs.tmp, kin, kout, iin, iout, m, s);
-            const u64 cnt = read_dev<unsigned long long>(counters + 8, s);
-            const u64 mine = cnt > (u64)rank ? (cnt - rank + world - 1) / world : 0;
-            cs.n_items2 = mine;
-            cs.launches += 5;
-            if (mine) {
-                // T+ upper bound for the global-scratch fallback
-                k_max_u32<<<grid1d(cnt, 256, sms), 256, 0, s>>>(nullptr, iout, cnt, g, (unsigned*)(counters + 9));
-                u32 maxls = (u32)read_dev<unsigned long long>(counters + 9, s);
-                u32* mylist = iin; // reuse
-                k_take_rank<<<grid1d(mine, 256, sms), 256, 0, s>>>(iout, 0, cnt, rank, world, mylist);
+            dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
+            cs.launches += 2 + 10;
+            const u64 nbig = read_dev<unsigned long long>(counters + 12, s);
+            const u64 nsmall = read_dev<unsigned long long>(counters + 13, s);
+            const u64 mybig = rank_share(nbig, rank, world);
+            const u64 mysmall = rank_share(nsmall, rank, world);
+            u32* lbig = iin;
+            u32* lsmall = iin + mybig;
+            if (mybig) {
+                const u32 kmax = (u32)read_dev(kout, s);
+                k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
                 GL_LAUNCH_CHECK();
                 const unsigned blocks = (unsigned)sms * 2;
-                u32 gcap = 0;
-                if (maxls > (u32)kCliqueCap) {
-                    gcap = maxls;
-                    cs.scratch.alloc((u64)blocks * kCliqueWarps * 5ull * gcap * sizeof(u32));
+                u64 gstride = 0;
+                if (kmax > (u32)kHSmemMax) {
+                    gstride = 3ull * kmax + 1 + (u64)kmax * ((kmax + 31) / 32);
+                    cs.scratch.alloc((u64)blocks * gstride * sizeof(u32));
                 }
-                const size_t smem = (size_t)kCliqueWarps * 5 * kCliqueCap * sizeof(u32);
-                GL_CUDA(cudaFuncSetAttribute(k_clique, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_clique<<<blocks, kCliqueWarps * 32, smem, s>>>(g, mylist, mine, counters + 0, d_partials,
-                                                                  gcap ? cs.scratch.as<u32>() : nullptr, gcap,
-                                                                  counters + 16);
+                const u32 ks = (u32)kHSmemMax;
+                const size_t smem = (size_t)(3ull * ks + 1 + (u64)ks * ((ks + 31) / 32)) * sizeof(u32);
+                GL_CUDA(cudaFuncSetAttribute(k_hclique_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                k_hclique_block<<<blocks, kHBlockThreads, smem, s>>>(
+                    g, lbig, mybig, counters + 0, cs.t.as<u32>(), d_partials,
+                    gstride ? cs.scratch.as<u32>() : nullptr, gstride);
                 GL_LAUNCH_CHECK();
-                cs.launches += 3;
+                cs.launches += 2;
+            }
+            if (mysmall) {
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig, nsmall, rank, world, lsmall);
+                GL_LAUNCH_CHECK();
+                k_hclique_warp<<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
+                    g, lsmall, mysmall, counters + 3, cs.t.as<u32>(), d_partials);
+                GL_LAUNCH_CHECK();
+                cs.launches += 2;
             }
         }
+        GL_CUDA(cudaEventRecord(tm.ev[1], s));
         GL_CUDA(cudaEventRecord(tm.ev[2], s));
 
         // cycles: top vertices, split small (warp hash) / big (block windows)
@@ -803,11 +901,9 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             const u64 nbig = read_dev<unsigned long long>(counters + 10, s);
             const u64 nsmall = read_dev<unsigned long long>(counters + 11, s);
             cs.work[2] = 8 * read_dev(cs.wpre.as<u64>() + m, s) / (u64)world; // c id + eid per wedge
-            cs.launches += 3;
-            const u64 mybig = nbig > (u64)rank ? (nbig - rank + world - 1) / world : 0;
-            const u64 mysmall = nsmall > (u64)rank ? (nsmall - rank + world - 1) / world : 0;
-            cs.n_items3b = mybig;
-            cs.n_items3s = mysmall;
+            cs.launches += 2 + 10;
+            const u64 mybig = rank_share(nbig, rank, world);
+            const u64 mysmall = rank_share(nsmall, rank, world);
             u32* lbig = iin;
             u32* lsmall = iin + mybig;
             if (mybig) {
@@ -816,9 +912,9 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 u32 cap = g.dmax + 1;
                 const unsigned blocks = (unsigned)sms;
                 cs.cursor.alloc((u64)blocks * 2 * cap * sizeof(u32));
-                const size_t smem = (size_t)(kWindow + kChunk + 1) * sizeof(u32);
+                const size_t smem = (size_t)kWindow * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_cycle_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_cycle_big<<<blocks, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1, d_partials,
+                k_cycle_big<<<blocks, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1, cs.slots.as<i64>(),
                                                               cs.cursor.as<u32>(), cap);
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
@@ -829,26 +925,53 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_cycle_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 k_cycle_small<<<(unsigned)sms * 3, kCycleSmallWarps * 32, smem, s>>>(
-                    g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, d_partials);
+                    g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, cs.slots.as<i64>());
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
             }
+            k_fold_slots<<<grid1d(m, 256, sms), 256, 0, s>>>(g, cs.slots.as<i64>(), d_partials);
+            GL_LAUNCH_CHECK();
+            cs.launches += 1;
         }
     }
     GL_CUDA(cudaEventRecord(tm.ev[3], s));
     GL_CUDA(cudaEventSynchronize(tm.ev[3]));
     GL_CUDA(cudaEventElapsedTime(&cs.ms[0], tm.ev[0], tm.ev[1]));
-    GL_CUDA(cudaEventElapsedTime(&cs.ms[1], tm.ev[1], tm.ev[2]));
     GL_CUDA(cudaEventElapsedTime(&cs.ms[2], tm.ev[2], tm.ev[3]));
-    if (m) cs.work[1] = 4 * read_dev<unsigned long long>(counters + 16, s);
+    cs.ms[1] = 0;
     cs.began = true;
+}
+
+// Phase B: triangle sums S (needs the complete t on this rank).
+void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
+    GL_CUDA(cudaSetDevice(gr.device));
+    if (!s) s = gr.stream;
+    CountState& cs = gr.cs;
+    if (!cs.began) throw state_error("gl_count_mid before gl_count_begin");
+    const DevGraph& g = gr.d;
+    const int sms = num_sms(gr.device);
+    Timer tm(2);
+    GL_CUDA(cudaEventRecord(tm.ev[0], s));
+    const u64 P = cs.probes;
+    const u64 b = P * (u64)cs.rank / cs.world, en = P * (u64)(cs.rank + 1) / cs.world;
+    if (g.m && en > b) {
+        unsigned gs = (unsigned)std::min<u64>((en - b + kTriTile - 1) / kTriTile, (u64)sms * 8);
+        k_trisum<<<gs, kTriThreads, 0, s>>>(g, cs.pre1.as<u64>(), b, en, cs.t.as<u32>(), d_partials);
+        GL_LAUNCH_CHECK();
+        cs.launches += 1;
+        cs.work[1] = (u64)((double)(4 * cs.lsum) * (double)(en - b) / (double)P);
+    }
+    GL_CUDA(cudaEventRecord(tm.ev[1], s));
+    GL_CUDA(cudaEventSynchronize(tm.ev[1]));
+    GL_CUDA(cudaEventElapsedTime(&cs.ms[1], tm.ev[0], tm.ev[1]));
+    cs.mid_done = true;
 }
 
 void count_finish(Graph& gr, const i64* d_part_shard, u64 begin, u64 end, u128 C[17], cudaStream_t s) {
     GL_CUDA(cudaSetDevice(gr.device));
     if (!s) s = gr.stream;
     CountState& cs = gr.cs;
-    if (!cs.began) throw state_error("gl_count_finish before gl_count_begin");
+    if (!cs.began || !cs.mid_done) throw state_error("gl_count_finish before gl_count_begin/gl_count_mid");
     const DevGraph& g = gr.d;
     if (end > g.m) end = g.m;
     if (begin > end) throw invalid_argument("edge_begin > edge_end");

@@ -60,9 +60,9 @@ struct DevBuf {
 // Per-graph counting state (device arrays reused across calls).
 struct CountState {
     DevBuf t;        // u32[m]   triangles per edge
-    DevBuf tplus;    // u32[m]   triangles with this edge as the lowest pair
     DevBuf x7, x10;  // u64[m]   micro outputs of the last shard
     DevBuf part;     // i64[2m]  partials for the single-process path
+    DevBuf slots;    // i64[2m]  C4 credits per adjacency slot (folded into y)
     DevBuf pre1;     // u64[m+1] probe prefix for the triangle kernels
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3b; // work lists
@@ -71,6 +71,9 @@ struct CountState {
     u64 shard_begin = 0, shard_end = 0;
     bool have_micro = false;
     bool began = false;
+    bool mid_done = false;
+    int rank = 0, world = 1;
+    u64 probes = 0, lsum = 0;
     float ms[5] = {0, 0, 0, 0, 0};
     u32 launches = 0;
     u64 work[4] = {0, 0, 0, 0};
@@ -93,6 +96,7 @@ void generate_rmat_device(const RmatParams& p, u64 count, u64* d_pairs, cudaStre
 
 // count.cu
 void count_begin(Graph& g, int rank, int world, i64* d_partials, cudaStream_t s);
+void count_mid(Graph& g, i64* d_partials, cudaStream_t s);
 void count_finish(Graph& g, const i64* d_partials, u64 begin, u64 end, u128 C[17],
                   cudaStream_t s);
 void micro_records(const Graph& g, u64 first, u64 count, u64* host_out /* count*10 */);

@@ -74,17 +74,56 @@ def exchange_partials(partials, world: int, group=None):
     return partials[rank * shard2:(rank + 1) * shard2].clone()
 
 
+def allreduce_triangles(graph, world: int, group=None, stream=None):
+    """Sum the per-edge uint32 triangle counts in place across ranks."""
+    if world == 1:
+        return
+    import torch
+    import torch.distributed as dist
+    ptr, m = graph.triangle_counts_device()
+    if m == 0:
+        return
+    dev = torch.device("cuda", graph.device)
+    # uint32 counts are summed as int32 (wrap-around is exact mod 2^32 and
+    # every final count is < 2^32): view the library buffer as a tensor.
+    t = _tensor_from_ptr(ptr, m, torch.int32, dev)
+    with torch.cuda.stream(stream or torch.cuda.current_stream(dev)):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def _tensor_from_ptr(ptr: int, n: int, dtype, device):
+    """Zero-copy torch view of library-owned device memory (DLPack-free)."""
+    import torch
+    class _Arr:
+        pass
+    a = _Arr()
+    a.__cuda_array_interface__ = {"shape": (n,), "typestr": torch.empty(0, dtype=dtype).numpy().dtype.str,
+                                  "data": (ptr, False), "version": 3, "strides": None}
+    return torch.as_tensor(a, device=device)
+
+
+def sharded_step(graph, partials, rank: int, world: int, stream, group=None):
+    """One full count with this rank's share of the work (see the C-ABI
+    sequence in include/graphlet_b200.h).  `partials`: int64 device tensor of
+    2*graph.partials_len(world).  Returns (X, (edge_begin, edge_end))."""
+    import torch
+    from . import global_from_unrestricted
+    dev = partials.device
+    graph.count_begin(rank, world, partials.data_ptr(), stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        allreduce_triangles(graph, world, group, stream=stream)
+        graph.count_mid(partials.data_ptr(), stream.cuda_stream)
+        shard = exchange_partials(partials, world, group)
+        b, e = shard_range(graph.num_edges(), world, rank)
+        C = graph.count_finish(shard.data_ptr(), b, e, stream.cuda_stream)
+        Ctot = allreduce_u128(C, group, device=dev) if world > 1 else C
+    return global_from_unrestricted(Ctot, graph.num_vertices(), graph.num_edges()), (b, e)
+
+
 def count_sharded(graph, rank: int, world: int, group=None, stream=None):
     """Full sharded count on this rank's GPU. Returns (X, (edge_begin, edge_end))."""
     import torch
-    from . import global_from_unrestricted
     dev = torch.device("cuda", graph.device)
-    plen = graph.partials_len(world)
-    partials = torch.empty(2 * plen, dtype=torch.int64, device=dev)
+    partials = torch.empty(2 * graph.partials_len(world), dtype=torch.int64, device=dev)
     s = torch.cuda.current_stream(dev) if stream is None else stream
-    graph.count_begin(rank, world, partials.data_ptr(), s.cuda_stream)
-    shard = exchange_partials(partials, world, group)
-    b, e = shard_range(graph.num_edges(), world, rank)
-    C = graph.count_finish(shard.data_ptr(), b, e, s.cuda_stream)
-    Ctot = allreduce_u128(C, group, device=dev) if world > 1 else C
-    return global_from_unrestricted(Ctot, graph.num_vertices(), graph.num_edges()), (b, e)
+    return sharded_step(graph, partials, rank, world, s, group)

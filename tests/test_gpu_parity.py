@@ -125,10 +125,10 @@ def test_edge_cases(cuda_device):
     assert sorted(g.labels().tolist()) == sorted({0, 3, 10**15, 2**64 - 1})
 
 
-@pytest.mark.parametrize("n", [5, 12, 40, 600])
+@pytest.mark.parametrize("n", [5, 12, 40, 600, 800])
 def test_complete_graphs_closed_form(cuda_device, n):
     """K_n: X3=C(n,3), X7=C(n,4); per edge t=n-2, x7=C(n-2,2), x10=0.
-    K_600 drives T+ = 598 > the 512-entry shared-memory stage (global path)."""
+    K_800 drives |U(a)| = 799 > the 768-member shared-memory H_a stage (global path)."""
     pairs = [(a, b) for a in range(n) for b in range(a + 1, n)]
     g, res, rec = gpu_count(pairs, cuda_device)
     X = res.X
@@ -168,11 +168,20 @@ def test_sharded_equals_single(cuda_device):
     full_rec = g.micro_records()
     world = 2
     plen = g.partials_len(world)
-    parts = []
+    parts, tris = [], []
     for rank in range(world):
         buf = torch.empty(2 * plen, dtype=torch.int64, device="cuda")
         g.count_begin(rank, world, buf.data_ptr())
+        ptr, m = g.triangle_counts_device()
+        tris.append(_copy_u32(ptr, m))
         parts.append(buf)
+    # all-reduce of t (emulated), then each rank's share of the triangle sums
+    tsum = tris[0] + tris[1]
+    for rank in range(world):
+        g.count_begin(rank, world, parts[rank].data_ptr())
+        ptr, m = g.triangle_counts_device()
+        _write_u32(ptr, tsum)
+        g.count_mid(parts[rank].data_ptr())
     total = parts[0] + parts[1]
     torch.cuda.synchronize()
     from paper_1608_05138_b200.dist import shard_range
@@ -187,6 +196,18 @@ def test_sharded_equals_single(cuda_device):
     assert gl.global_from_unrestricted(Csum, g.num_vertices(), g.num_edges()) == full.X
     assert Csum == full.C
     assert np.array_equal(np.concatenate(recs), full_rec)
+
+
+def _copy_u32(ptr, m):
+    from paper_1608_05138_b200.dist import _tensor_from_ptr
+    import torch
+    return _tensor_from_ptr(ptr, m, torch.int32, torch.device("cuda", 0)).clone()
+
+
+def _write_u32(ptr, src):
+    from paper_1608_05138_b200.dist import _tensor_from_ptr
+    import torch
+    _tensor_from_ptr(ptr, src.numel(), torch.int32, torch.device("cuda", 0)).copy_(src)
 
 
 def test_device_generated_graph_matches_host(cuda_device):

@@ -472,26 +472,52 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
     }
 }
 
-// Big tops: one block per top vertex a, dense W windows in shared memory.
-// Work inside a window is expanded per warp tile of 32 lower neighbours b:
-// lane i owns b_i's run N(b_i) n [lo,hi) (cursor-resumed), the tile's runs
-// are prefix-summed with shuffles and every lane then walks consecutive
-// wedges, finding its owner lane by a 5-step shuffle search.  Credits go to
-// per-adjacency-slot accumulators (consecutive slots of one row are
-// consecutive addresses), folded into edge rows by k_fold_slots.
+// Big tops: one block per top vertex a, dense W windows over c in shared
+// memory (16-bit packed counters when |L(a)| < 65536: 64K c-values per
+// window, else 32-bit: 32K).  Per window the non-empty runs
+// N(b) n [lo,hi) of the lower neighbours b are compacted (flag scan) and
+// prefix-summed in per-block global scratch; the wedges are then flattened
+// block-wide: each warp takes rounds of 32 consecutive wedges, finds the
+// round's first run with one warp-uniform binary search and each lane's run
+// among the next 32 (all non-empty) with a 5-step shuffle search.  Credits go
+// to per-adjacency-slot accumulators (consecutive wedges of a run are
+// consecutive slots), folded into edge rows by k_fold_slots.
+
+__device__ __forceinline__ void w_inc(u32* W, u32 i, bool half) {
+    if (half)
+        atomicAdd(&W[i >> 1], 1u << ((i & 1) << 4));
+    else
+        atomicAdd(&W[i], 1u);
+}
+__device__ __forceinline__ u32 w_get(const u32* W, u32 i, bool half) {
+    return half ? (W[i >> 1] >> ((i & 1) << 4)) & 0xffffu : W[i];
+}
+
+// per-block scratch layout (cap = dmax + 1 entries each)
+struct BigScratch {
+    u32 *cur, *hpos, *pre, *rj;
+    u64* rs;
+};
+__device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
+    BigScratch s;
+    s.cur = base;
+    s.hpos = base + cap;
+    s.pre = base + 2 * (u64)cap;
+    s.rj = base + 3 * (u64)cap + 1;
+    s.rs = reinterpret_cast<u64*>(base + 4 * (u64)cap + 2); // cap*2 words, 8B aligned by construction
+    return s;
+}
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 6ull * cap + 4; }
+
 __global__ void __launch_bounds__(kBigThreads, 1)
 k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-            i64* __restrict__ slot_acc, u32* __restrict__ gcur, u32 gcur_cap) {
-    extern __shared__ u32 W[]; // kWindow counters
+            i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
+    extern __shared__ u32 W[]; // kWindow words
     __shared__ unsigned long long s_idx;
     __shared__ u32 s_next;
-    __shared__ unsigned long long s_total;
-    __shared__ unsigned long long s_bsum[kBigThreads / 32][32];
     const u32 lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    u32* cur = gcur + (u64)blockIdx.x * 2 * gcur_cap;
-    u32* hpos = cur + gcur_cap;
+    BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
     for (u32 i = threadIdx.x; i < kWindow; i += blockDim.x) W[i] = 0;
-    s_bsum[wid][lane] = 0;
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
@@ -502,99 +528,99 @@ k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lon
         const u64 E0 = g.loff[a];
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
+        const bool half = nb < 65536u;
+        const u32 span = half ? 2u * kWindow : (u32)kWindow;
         if (threadIdx.x == 0) s_next = kEmpty;
         __syncthreads();
         for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
-            cur[j] = 0;
+            S.cur[j] = 0;
             const u64 e = E0 + j;
             if (g.epos[e] > 0) atomicMin(&s_next, g.adj[g.off[g.eu[e]]]);
         }
         __syncthreads();
         u32 lo = s_next;
         while (lo != kEmpty && lo < a) {
-            const u32 hi = (u64)lo + kWindow < (u64)a ? lo + kWindow : a;
-            if (threadIdx.x == 0) s_total = 0;
-            __syncthreads();
-            u64 mytot = 0;
+            const u32 hi = (u64)lo + span < (u64)a ? lo + span : a;
+            // runs [cur, hpos) of every b; flag non-empty ones
             for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
                 const u64 e = E0 + j;
                 const u64 rb = g.off[g.eu[e]];
-                const u32 c0 = cur[j];
+                const u32 c0 = S.cur[j];
                 const u64 p = lower_bound_dev<u32, u64>(g.adj, rb + c0, rb + g.epos[e], hi);
-                hpos[j] = (u32)(p - rb);
-                mytot += p - rb - c0;
+                S.hpos[j] = (u32)(p - rb);
+                S.pre[j] = p - rb > c0 ? 1u : 0u;
             }
-            mytot = warp_sum_u64(mytot);
-            if (lane == 0 && mytot) atomicAdd(&s_total, (unsigned long long)mytot);
             __syncthreads();
-            const bool bulk_clear = s_total > (unsigned long long)(kWindow / 4);
+            const u32 nnz = block_exclusive_scan<kBigThreads>(S.pre, nb);
+            // compact: run j -> position pre[j]; hpos still holds the run ends
+            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
+                const u32 c0 = S.cur[j], h = S.hpos[j];
+                if (h > c0) {
+                    const u32 q = S.pre[j];
+                    S.rj[q] = j;
+                    S.rs[q] = g.off[g.eu[E0 + j]] + c0;
+                }
+            }
+            __syncthreads();
+            // run lengths in compacted order, then their prefix (reusing pre)
+            for (u32 q = threadIdx.x; q < nnz; q += blockDim.x) {
+                const u32 j = S.rj[q];
+                S.pre[q] = S.hpos[j] - S.cur[j];
+            }
+            __syncthreads();
+            const u32 T = block_exclusive_scan<kBigThreads>(S.pre, nnz);
+            if (threadIdx.x == 0) S.pre[nnz] = T;
+            __syncthreads();
+            const bool bulk_clear = T > (u32)(kWindow / 8);
             for (int pass = 0; pass < (bulk_clear ? 2 : 3); ++pass) {
-                for (u32 tile = wid * 32; tile < nb; tile += nwarps * 32) {
-                    const u32 j = tile + lane;
-                    u64 rs = 0;
-                    u32 len = 0;
-                    if (j < nb) {
-                        const u64 e = E0 + j;
-                        const u32 c0 = cur[j];
-                        rs = g.off[g.eu[e]] + c0;
-                        len = hpos[j] - c0;
-                    }
-                    u32 incl = len;
+                for (u32 k0 = wid * 32; k0 < T; k0 += nwarps * 32) {
+                    const u32 bs = upper_bound_dev<u32, u32>(S.pre, 0, nnz + 1, k0) - 1; // warp-uniform
+                    const u32 k = k0 + lane;
+                    const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
+                    u32 owner = 0;
 #pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
-                        if (lane >= (u32)d) incl += o;
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const u32 cand = owner + step;
+                        const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
+                        if (cand < 32 && ex <= k) owner = cand;
                     }
-                    const u32 excl = incl - len;
-                    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
-                    for (u32 base = 0; base < total; base += 32) {
-                        const u32 k = base + lane;
-                        u32 owner = 0;
-#pragma unroll
-                        for (int step = 16; step > 0; step >>= 1) {
-                            const u32 cand = owner + step;
-                            const u32 ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                            if (cand < 32 && ex <= k) owner = cand;
-                        }
-                        const u32 oex = __shfl_sync(0xffffffffu, excl, owner);
-                        const u64 ors = __shfl_sync(0xffffffffu, rs, owner);
-                        if (k < total) {
-                            const u64 slot = ors + (k - oex);
-                            const u32 cv = g.adj[slot];
-                            if (pass == 0) {
-                                atomicAdd(&W[cv - lo], 1u);
-                            } else if (pass == 1) {
-                                const u32 val = W[cv - lo] - 1;
-                                if (val) {
-                                    atomic_add_i64(&slot_acc[slot], (i64)val);
-                                    atomicAdd(&s_bsum[wid][owner], (unsigned long long)val);
-                                }
-                            } else {
-                                W[cv - lo] = 0;
-                            }
+                    const u32 q = bs + owner;
+                    const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
+                    u64 key = ~0ull, val = 0;
+                    if (k < T) {
+                        const u64 slot = S.rs[q] + (k - opi);
+                        const u32 ci = g.adj[slot] - lo;
+                        if (pass == 0) {
+                            w_inc(W, ci, half);
+                        } else if (pass == 1) {
+                            val = w_get(W, ci, half) - 1;
+                            key = q;
+                            if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
+                        } else {
+                            if (half)
+                                W[ci >> 1] = 0;
+                            else
+                                W[ci] = 0;
                         }
                     }
                     if (pass == 1) {
-                        __syncwarp();
-                        const unsigned long long bs = s_bsum[wid][lane];
-                        if (bs) {
-                            atomic_add_i64(&slot_acc[abase + j], (i64)bs);
-                            s_bsum[wid][lane] = 0;
-                        }
-                        __syncwarp();
+                        u64 sum;
+                        const bool tail = seg_tail_sum(key, val, &sum);
+                        if (k < T && tail && sum) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)sum);
                     }
                 }
                 __syncthreads();
             }
             if (bulk_clear) {
-                for (u32 i = threadIdx.x; i < hi - lo; i += blockDim.x) W[i] = 0;
+                const u32 words = half ? (hi - lo + 1) >> 1 : hi - lo;
+                for (u32 i = threadIdx.x; i < words; i += blockDim.x) W[i] = 0;
             }
             // advance cursors, next non-empty window start
             if (threadIdx.x == 0) s_next = kEmpty;
             __syncthreads();
             for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
-                const u32 h = hpos[j];
-                cur[j] = h;
+                const u32 h = S.hpos[j];
+                S.cur[j] = h;
                 const u64 e = E0 + j;
                 if (h < g.epos[e]) atomicMin(&s_next, g.adj[g.off[g.eu[e]] + h]);
             }
@@ -909,9 +935,9 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             if (mybig) {
                 k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
                 GL_LAUNCH_CHECK();
-                u32 cap = g.dmax + 1;
+                u32 cap = g.dmax + 2;
                 const unsigned blocks = (unsigned)sms;
-                cs.cursor.alloc((u64)blocks * 2 * cap * sizeof(u32));
+                cs.cursor.alloc((u64)blocks * ((big_scratch_words(cap) + 1) & ~1ull) * sizeof(u32));
                 const size_t smem = (size_t)kWindow * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_cycle_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 k_cycle_big<<<blocks, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1, cs.slots.as<i64>(),

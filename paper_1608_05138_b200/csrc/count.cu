@@ -926,7 +926,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
             const u64 nbig = read_dev<unsigned long long>(counters + 10, s);
             const u64 nsmall = read_dev<unsigned long long>(counters + 11, s);
-            cs.work[2] = 8 * read_dev(cs.wpre.as<u64>() + m, s) / (u64)world; // c id + eid per wedge
+            cs.work[2] = 12 * read_dev(cs.wpre.as<u64>() + m, s) / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);

@@ -493,6 +493,20 @@ __device__ __forceinline__ u32 w_get(const u32* W, u32 i, bool half) {
     return half ? (W[i >> 1] >> ((i & 1) << 4)) & 0xffffu : W[i];
 }
 
+// first index in [lo, hi) with a[idx] >= x, galloping from lo: runs inside a
+// window are usually a handful of entries, so this costs ~log2(run) loads.
+__device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64 lo, u64 hi, u32 x) {
+    if (lo >= hi || a[lo] >= x) return lo;
+    u64 step = 1, base = lo;
+    for (;;) {
+        const u64 probe = base + step;
+        if (probe >= hi) return lower_bound_dev<u32, u64>(a, base + 1, hi, x);
+        if (a[probe] >= x) return lower_bound_dev<u32, u64>(a, base + 1, probe, x);
+        base = probe;
+        step <<= 1;
+    }
+}
+
 // per-block scratch layout (cap = dmax + 1 entries each)
 struct BigScratch {
     u32 *cur, *hpos, *pre, *rj;
@@ -546,7 +560,7 @@ k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lon
                 const u64 e = E0 + j;
                 const u64 rb = g.off[g.eu[e]];
                 const u32 c0 = S.cur[j];
-                const u64 p = lower_bound_dev<u32, u64>(g.adj, rb + c0, rb + g.epos[e], hi);
+                const u64 p = gallop_lower_bound(g.adj, rb + c0, rb + g.epos[e], hi);
                 S.hpos[j] = (u32)(p - rb);
                 S.pre[j] = p - rb > c0 ? 1u : 0u;
             }
@@ -572,41 +586,97 @@ k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lon
             if (threadIdx.x == 0) S.pre[nnz] = T;
             __syncthreads();
             const bool bulk_clear = T > (u32)(kWindow / 8);
+            // each warp walks a contiguous range of wedges: one binary search
+            // per pass, then the run pointer advances by ballot
+            const u32 per = ((T + nwarps * 32 - 1) / (nwarps * 32)) * 32;
+            const u32 kb = wid * per, ke = kb + per < T ? kb + per : T;
             for (int pass = 0; pass < (bulk_clear ? 2 : 3); ++pass) {
-                for (u32 k0 = wid * 32; k0 < T; k0 += nwarps * 32) {
-                    const u32 bs = upper_bound_dev<u32, u32>(S.pre, 0, nnz + 1, k0) - 1; // warp-uniform
-                    const u32 k = k0 + lane;
-                    const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
-                    u32 owner = 0;
+                if (kb < ke) {
+                    // round state: run pointer bs, the 32 run starts pi, each
+                    // lane's run q, slot and neighbour id cv.  The next round's
+                    // mapping and adjacency load are issued before this
+                    // round's atomics (software pipelining).
+                    u32 bs = upper_bound_dev<u32, u32>(S.pre, 0, nnz + 1, kb) - 1; // warp-uniform
+                    u32 k0 = kb;
+                    u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
+                    u32 q;
+                    u64 slot = 0;
+                    u32 cv = 0;
+                    {
+                        const u32 k = k0 + lane;
+                        u32 owner = 0;
 #pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const u32 cand = owner + step;
-                        const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
-                        if (cand < 32 && ex <= k) owner = cand;
-                    }
-                    const u32 q = bs + owner;
-                    const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
-                    u64 key = ~0ull, val = 0;
-                    if (k < T) {
-                        const u64 slot = S.rs[q] + (k - opi);
-                        const u32 ci = g.adj[slot] - lo;
-                        if (pass == 0) {
-                            w_inc(W, ci, half);
-                        } else if (pass == 1) {
-                            val = w_get(W, ci, half) - 1;
-                            key = q;
-                            if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
-                        } else {
-                            if (half)
-                                W[ci >> 1] = 0;
-                            else
-                                W[ci] = 0;
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const u32 cand = owner + step;
+                            const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
+                            if (cand < 32 && ex <= k) owner = cand;
+                        }
+                        q = bs + owner;
+                        const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
+                        if (k < ke) {
+                            slot = S.rs[q] + (k - opi);
+                            cv = g.adj[slot];
                         }
                     }
-                    if (pass == 1) {
-                        u64 sum;
-                        const bool tail = seg_tail_sum(key, val, &sum);
-                        if (k < T && tail && sum) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)sum);
+                    for (;;) {
+                        const u32 kn = k0 + 32;
+                        const bool more = kn < ke;
+                        u32 n_bs = bs, n_pi = pi, n_q = 0, n_cv = 0;
+                        u64 n_slot = 0;
+                        if (more) {
+                            unsigned bal = __ballot_sync(0xffffffffu, pi <= kn);
+                            while (bal == 0xffffffffu) {
+                                n_bs += 31;
+                                n_pi = n_bs + lane <= nnz ? S.pre[n_bs + lane] : 0xffffffffu;
+                                bal = __ballot_sync(0xffffffffu, n_pi <= kn);
+                            }
+                            n_bs += 31 - __clz(bal);
+                            n_pi = n_bs + lane <= nnz ? S.pre[n_bs + lane] : 0xffffffffu;
+                            const u32 k = kn + lane;
+                            u32 owner = 0;
+#pragma unroll
+                            for (int step = 16; step > 0; step >>= 1) {
+                                const u32 cand = owner + step;
+                                const u32 ex = __shfl_sync(0xffffffffu, n_pi, cand & 31);
+                                if (cand < 32 && ex <= k) owner = cand;
+                            }
+                            n_q = n_bs + owner;
+                            const u32 opi = __shfl_sync(0xffffffffu, n_pi, owner);
+                            if (k < ke) {
+                                n_slot = S.rs[n_q] + (k - opi);
+                                n_cv = g.adj[n_slot];
+                            }
+                        }
+                        // process this round
+                        const bool valid = k0 + lane < ke;
+                        u64 key = ~0ull, val = 0;
+                        if (valid) {
+                            const u32 ci = cv - lo;
+                            if (pass == 0) {
+                                w_inc(W, ci, half);
+                            } else if (pass == 1) {
+                                val = w_get(W, ci, half) - 1;
+                                key = q;
+                                if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
+                            } else {
+                                if (half)
+                                    W[ci >> 1] = 0;
+                                else
+                                    W[ci] = 0;
+                            }
+                        }
+                        if (pass == 1) {
+                            u64 sum;
+                            const bool tail = seg_tail_sum(key, val, &sum);
+                            if (valid && tail && sum) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)sum);
+                        }
+                        if (!more) break;
+                        k0 = kn;
+                        bs = n_bs;
+                        pi = n_pi;
+                        q = n_q;
+                        slot = n_slot;
+                        cv = n_cv;
                     }
                 }
                 __syncthreads();

@@ -292,18 +292,64 @@ __device__ u32 block_exclusive_scan(u32* a, u32 n) {
     return s_carry;
 }
 
+// Walk items [kb, ke) of a run-length list with one warp (pre = exclusive
+// prefix over n runs, pre[n] = total): one binary search, then per round of
+// 32 items a 5-step shuffle search for each lane's run and a ballot to
+// advance the run pointer.  f(valid, run, offset) is called converged.
+template <typename F>
+__device__ __forceinline__ void warp_walk(const u32* pre, u32 n, u32 kb, u32 ke, F&& f) {
+    const u32 lane = lane_id();
+    if (kb >= ke) return;
+    u32 bs = upper_bound_dev<u32, u32>(pre, 0, n + 1, kb) - 1;
+    for (u32 k0 = kb; k0 < ke; k0 += 32) {
+        const u32 k = k0 + lane;
+        u32 pi = bs + lane <= n ? pre[bs + lane] : 0xffffffffu;
+        u32 owner = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const u32 cand = owner + step;
+            const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
+            if (cand < 32 && ex <= k) owner = cand;
+        }
+        const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
+        f(k < ke, bs + owner, k - opi);
+        const u32 kn = k0 + 32;
+        if (kn < ke) {
+            unsigned bal = __ballot_sync(0xffffffffu, pi <= kn);
+            while (bal == 0xffffffffu) {
+                bs += 31;
+                pi = bs + lane <= n ? pre[bs + lane] : 0xffffffffu;
+                bal = __ballot_sync(0xffffffffu, pi <= kn);
+            }
+            bs += 31 - __clz(bal);
+        }
+    }
+}
+
 __device__ __forceinline__ u64 hblock_ws_words(u32 k) {
     return 3ull * k + 1 + (u64)k * ((k + 31) >> 5);
 }
 
+// k > 32: one block per vertex a.  Phase 1 builds H_a's bitmap rows by one
+// probe per (member i, candidate) -- contiguous ranges per warp -- and appends
+// every H-edge (i, j, eid) to a per-block list; phase 2 streams that list:
+// popcount of the two rows, one t and one x7 credit per H-edge; phase 3
+// credits the edges (a, x_i).
 __global__ void __launch_bounds__(kHBlockThreads)
 k_hclique_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-                u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride) {
+                u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
+                uint2* __restrict__ hlist_all, u64 hcap) {
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
+    __shared__ u32 s_nh;
+    const u32 lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    uint2* hlist = hlist_all + (u64)blockIdx.x * hcap;
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
+        if (threadIdx.x == 0) {
+            s_idx = atomicAdd(queue, 1ull);
+            s_nh = 0;
+        }
         __syncthreads();
         const unsigned long long idx = s_idx;
         if (idx >= n_items) break;
@@ -329,54 +375,54 @@ k_hclique_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned
         const u32 Q = block_exclusive_scan<kHBlockThreads>(pre, k);
         if (threadIdx.x == 0) pre[k] = Q;
         __syncthreads();
-        // phase 1: flattened probes set both mirror bits
-        for (u32 q = threadIdx.x; q < Q; q += blockDim.x) {
-            const u32 i = upper_bound_dev<u32, u32>(pre, 0, k + 1, q) - 1;
-            const u32 r = q - pre[i];
-            const u32 x = xs[i];
-            const u64 xb = u_begin(g, x), xe = g.off[x + 1];
-            u32 j;
-            bool found;
-            if (xe - xb <= (u64)(k - 1 - i)) {
-                const u32 y = g.adj[xb + r];
-                j = lower_bound_dev<u32, u32>(xs, i + 1, k, y);
-                found = j < k && xs[j] == y;
-            } else {
-                j = i + 1 + r;
-                const u32 y = xs[j];
-                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
-                found = p < xe && g.adj[p] == y;
-            }
-            if (found) {
-                atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
-                atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
-            }
+        // phase 1
+        {
+            const u32 per = ((Q + nwarps * 32 - 1) / (nwarps * 32)) * 32;
+            const u32 kb = wid * per, ke = kb + per < Q ? kb + per : Q;
+            warp_walk(pre, k, kb, ke, [&](bool valid, u32 i, u32 r) {
+                bool found = false;
+                u32 j = 0, e = 0;
+                if (valid) {
+                    const u32 x = xs[i];
+                    const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+                    if (xe - xb <= (u64)(k - 1 - i)) {
+                        const u32 y = g.adj[xb + r];
+                        j = lower_bound_dev<u32, u32>(xs, i + 1, k, y);
+                        found = j < k && xs[j] == y;
+                        if (found) e = g.eid[xb + r];
+                    } else {
+                        j = i + 1 + r;
+                        const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
+                        found = p < xe && g.adj[p] == xs[j];
+                        if (found) e = g.eid[p];
+                    }
+                    if (found) {
+                        atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
+                        atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
+                    }
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, found);
+                u32 base = 0;
+                if (lane == 0 && bal) base = atomicAdd(&s_nh, (u32)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (found) hlist[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
+            });
         }
         __syncthreads();
-        // phase 2: H-edges (i < j) by row word; popcount of row ANDs
-        for (u64 q = threadIdx.x; q < (u64)k * W; q += blockDim.x) {
-            const u32 i = (u32)(q / W), w = (u32)(q % W);
-            if (w < (i >> 5)) continue;
-            u32 bits = rows[q];
-            if (w == (i >> 5)) bits &= (i & 31) == 31 ? 0u : (~0u << ((i & 31) + 1));
-            if (!bits) continue;
-            const u32 x = xs[i];
-            const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+        // phase 2: stream the H-edges
+        const u32 nh = s_nh;
+        for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
+            const uint2 he = hlist[h];
+            const u32 i = he.x & 0xffffu, j = he.x >> 16;
             const u32* ri = rows + (u64)i * W;
-            while (bits) {
-                const u32 j = w * 32 + (__ffs(bits) - 1);
-                bits &= bits - 1;
-                const u32* rj = rows + (u64)j * W;
-                u32 c = 0;
-                for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
-                if (c) {
-                    atomicAdd(&tri[i], c);
-                    atomicAdd(&tri[j], c);
-                }
-                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
-                const u32 e = g.eid[p];
-                atomicAdd(&t[e], 1u);
-                if (c) atomic_add_i64(&part[2 * (u64)e], (i64)c);
+            const u32* rj = rows + (u64)j * W;
+            u32 c = 0;
+            for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
+            atomicAdd(&t[he.y], 1u);
+            if (c) {
+                atomicAdd(&tri[i], c);
+                atomicAdd(&tri[j], c);
+                atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
             }
         }
         __syncthreads();
@@ -796,16 +842,42 @@ __global__ void k_seq(u32* __restrict__ ids, u64 n) {
         ids[i] = (u32)i;
 }
 
-// |U(a)| for the H-pass work list (vertices with >= 2 up-neighbours)
+// H-pass work list key: big-k (k > 32) items first, each class ordered by its
+// probe count Q(a) = sum_i min(|U(x_i)|, k-1-i) (the phase-1 work).
+constexpr u64 kHBigFlag = 1ull << 40;
+__global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
+    u32 mx = 0;
+    for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
+        const u32 k = (u32)(g.off[a + 1] - (g.off[a] + g.lcnt[a]));
+        mx = k > mx ? k : mx;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        const u32 o = __shfl_down_sync(0xffffffffu, mx, d);
+        mx = o > mx ? o : mx;
+    }
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
 __global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* __restrict__ cnt) {
     unsigned long long lb = 0, ls = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
-        u64 k = g.off[a + 1] - (g.off[a] + g.lcnt[a]);
-        keys[a] = k >= 2 ? k : 0;
-        if (k > (u64)kHWarpMax)
-            ++lb;
-        else if (k >= 2)
-            ++ls;
+        const u64 ub = g.off[a] + g.lcnt[a];
+        const u64 k = g.off[a + 1] - ub;
+        u64 key = 0;
+        if (k >= 2) {
+            u64 q = 0;
+            for (u64 i = 0; i + 1 < k; ++i) {
+                const u32 x = g.adj[ub + i];
+                const u64 lu = g.off[x + 1] - (g.off[x] + g.lcnt[x]);
+                const u64 rem = k - 1 - i;
+                q += lu < rem ? lu : rem;
+            }
+            key = (k > (u64)kHWarpMax ? kHBigFlag : 0) | (q + 1);
+            if (k > (u64)kHWarpMax)
+                ++lb;
+            else
+                ++ls;
+        }
+        keys[a] = key;
     }
     if (lb) atomicAdd(&cnt[0], lb);
     if (ls) atomicAdd(&cnt[1], ls);
@@ -953,22 +1025,28 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* lbig = iin;
             u32* lsmall = iin + mybig;
             if (mybig) {
-                const u32 kmax = (u32)read_dev(kout, s);
+                const u64 qmax = (read_dev(kout, s) & (kHBigFlag - 1)) - 1;
                 k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
                 GL_LAUNCH_CHECK();
                 const unsigned blocks = (unsigned)sms * 2;
+                k_umax<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 14));
+                GL_LAUNCH_CHECK();
+                const u32 kmax = (u32)read_dev<unsigned long long>(counters + 14, s);
+                if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
                 u64 gstride = 0;
                 if (kmax > (u32)kHSmemMax) {
                     gstride = 3ull * kmax + 1 + (u64)kmax * ((kmax + 31) / 32);
                     cs.scratch.alloc((u64)blocks * gstride * sizeof(u32));
                 }
+                if (qmax >= (1ull << 32)) throw overflow_error("H-pass probe count exceeds 32 bits");
+                cs.hlist.alloc((u64)blocks * (qmax + 1) * sizeof(uint2));
                 const u32 ks = (u32)kHSmemMax;
                 const size_t smem = (size_t)(3ull * ks + 1 + (u64)ks * ((ks + 31) / 32)) * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_hclique_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
                 k_hclique_block<<<blocks, kHBlockThreads, smem, s>>>(
                     g, lbig, mybig, counters + 0, cs.t.as<u32>(), d_partials,
-                    gstride ? cs.scratch.as<u32>() : nullptr, gstride);
+                    gstride ? cs.scratch.as<u32>() : nullptr, gstride, cs.hlist.as<uint2>(), qmax + 1);
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
             }

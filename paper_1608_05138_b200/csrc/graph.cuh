@@ -63,6 +63,7 @@ struct CountState {
     DevBuf x7, x10;  // u64[m]   micro outputs of the last shard
     DevBuf part;     // i64[2m]  partials for the single-process path
     DevBuf slots;    // i64[2m]  C4 credits per adjacency slot (folded into y)
+    DevBuf hlist;    // per-block H-edge lists of the clique pass
     DevBuf pre1;     // u64[m+1] probe prefix for the triangle kernels
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3b; // work lists

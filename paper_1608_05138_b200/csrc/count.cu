@@ -42,8 +42,11 @@ constexpr int kTriTile = 2048;       // probes per block tile
 constexpr int kCycleSmallWarps = 8;  // warps per small-top block
 constexpr int kHashSlots = 1024;     // per-warp hash slots (small tops)
 constexpr u64 kSmallWedges = 512;    // small-top threshold (<= half the slots)
-constexpr int kBigThreads = 1024;    // block per big top
-constexpr int kWindow = 32768;       // dense W window (u32) in shared memory
+constexpr int kBigThreads = 1024;    // block per big top (dense windows), one block per SM
+constexpr int kMidThreads = 512;     // block per mid top (hash), two blocks per SM
+constexpr int kWindow = 32768;       // dense W window words (u32, or 2 x u16) in shared memory
+constexpr u32 kMidSlots = 16384;     // mid tops: block hash, u32 keys + u16 counts (96 KB)
+constexpr u64 kMidWedges = 8192;     // mid-top threshold (<= half the hash slots)
 
 constexpr u32 kEmpty = 0xffffffffu;
 
@@ -553,31 +556,191 @@ __device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64
     }
 }
 
-// per-block scratch layout (cap = dmax + 1 entries each)
+// per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
-    u32 *cur, *hpos, *pre, *rj;
-    u64* rs;
+    u32 *cur, *hpos, *rend, *pre, *rj;
+    u64 *rb, *rs;
 };
 __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     BigScratch s;
     s.cur = base;
     s.hpos = base + cap;
-    s.pre = base + 2 * (u64)cap;
-    s.rj = base + 3 * (u64)cap + 1;
-    s.rs = reinterpret_cast<u64*>(base + 4 * (u64)cap + 2); // cap*2 words, 8B aligned by construction
+    s.rend = base + 2 * (u64)cap;
+    s.pre = base + 3 * (u64)cap;              // cap + 1 entries
+    s.rj = base + 4 * (u64)cap + 1;
+    u64* q = reinterpret_cast<u64*>(base + ((5 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
+    s.rb = q;
+    s.rs = q + cap;
     return s;
 }
-__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 6ull * cap + 4; }
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 9ull * cap + 8; }
 
-__global__ void __launch_bounds__(kBigThreads, 1)
-k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-            i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
-    extern __shared__ u32 W[]; // kWindow words
+// W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
+// or an open-addressing hash over all c < a (mid tops, HASH).  Hash keys are
+// u32 (kEmpty = free), counts u16 packed two per word.
+__device__ __forceinline__ u32 mid_slot(u32 c) { return (c * 0x9E3779B1u) >> (32 - 14); }
+static_assert(kMidSlots == 16384, "mid_slot assumes 16384 slots");
+
+template <bool HASH>
+__device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, bool half) {
+    if (HASH) {
+        u32* keys = W;
+        u32 h = mid_slot(c);
+        for (;;) {
+            const u32 k = keys[h];
+            if (k == c) break;
+            if (k == kEmpty) {
+                const u32 prev = atomicCAS(&keys[h], kEmpty, c);
+                if (prev == kEmpty || prev == c) break;
+            }
+            h = (h + 1) & (kMidSlots - 1);
+        }
+        atomicAdd(&W[kMidSlots + (h >> 1)], 1u << ((h & 1) << 4));
+    } else {
+        w_inc(W, c - lo, half);
+    }
+}
+template <bool HASH>
+__device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, bool half) {
+    if (HASH) {
+        u32 h = mid_slot(c);
+        while (W[h] != c) h = (h + 1) & (kMidSlots - 1);
+        return (W[kMidSlots + (h >> 1)] >> ((h & 1) << 4)) & 0xffffu;
+    } else {
+        return w_get(W, c - lo, half);
+    }
+}
+// dense windows only: the hash is always bulk-cleared (a deleted key would
+// break the probe chains of the clears still to come)
+__device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, bool half) {
+    const u32 ci = c - lo;
+    if (half)
+        W[ci >> 1] = 0;
+    else
+        W[ci] = 0;
+}
+
+template <bool HASH, int PASS>
+__device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, bool half, i64* __restrict__ slot_acc, u64 slot,
+                                         u64& val) {
+    if (PASS == 0) {
+        tab_inc<HASH>(W, cv, lo, half);
+    } else if (PASS == 1) {
+        const u32 v = tab_get<HASH>(W, cv, lo, half) - 1u;
+        if (v) atomic_add_i64(&slot_acc[slot], (i64)v);
+        val = v;
+    } else {
+        tab_clear_one(W, cv, lo, half);
+    }
+}
+
+// One pass over a warp's range [kb, ke) of a window's flattened wedge list
+// (compacted runs q, S.pre = wedge prefix, run q = adjacency slots
+// [S.rs[q], S.rs[q] + len)).  Stretches of full 32-wedge rounds inside one
+// run take the uniform path: slot = base + lane, four rounds of loads in
+// flight, the (a,b) credit kept per lane and warp-reduced once per stretch.
+// Rounds that straddle runs take the mixed path: each lane finds its run
+// among the next 32 starts by a 5-step shuffle search and the (a,b) credit is
+// a segmented shuffle sum whose tail lanes issue the RED.
+//   PASS 0: W[c]++     PASS 1: credit W[c]-1 to (b,c) and, summed, to (a,b)
+//   PASS 2: W[c] = 0 (sparse clear of a dense window)
+template <bool HASH, int PASS>
+__device__ __forceinline__ void window_pass(const DevGraph& g, const BigScratch& S, u32 nnz, u32 kb, u32 ke, u32* W,
+                                            u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
+    const u32 lane = lane_id();
+    if (kb >= ke) return;
+    u32 bs = upper_bound_dev<u32, u32>(S.pre, 0, nnz + 1, kb) - 1; // warp-uniform
+    u32 k0 = kb;
+    while (k0 < ke) {
+        u32 e1 = S.pre[bs + 1];
+        while (e1 <= k0) e1 = S.pre[++bs + 1];
+        const u32 stop = e1 < ke ? e1 : ke;
+        if (stop - k0 >= 32u) {
+            // uniform stretch of full rounds inside run bs
+            const u32 nfull = (stop - k0) >> 5;
+            const u64 sbase = S.rs[bs] + (k0 - S.pre[bs]) + lane;
+            u64 acc = 0;
+            for (u32 r = 0; r < nfull; r += 4) {
+                u32 cv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cv[u] = r + u < nfull ? __ldg(g.adj + sbase + 32u * (r + u)) : kEmpty;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (cv[u] != kEmpty) {
+                        u64 v = 0;
+                        wedge_op<HASH, PASS>(W, cv[u], lo, half, slot_acc, sbase + 32u * (r + u), v);
+                        acc += v;
+                    }
+                }
+            }
+            if (PASS == 1) {
+                acc = warp_sum_u64(acc);
+                if (lane == 0 && acc) atomic_add_i64(&slot_acc[abase + S.rj[bs]], (i64)acc);
+            }
+            k0 += nfull << 5;
+        } else {
+            // mixed round [k0, k0 + 32)
+            const u32 k = k0 + lane;
+            const bool valid = k < ke;
+            const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
+            u32 owner = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const u32 cand = owner + step;
+                const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
+                if (cand < 32 && ex <= k) owner = cand;
+            }
+            const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
+            const u32 onx = __shfl_sync(0xffffffffu, pi, (owner + 1) & 31);
+            const u32 q = bs + owner;
+            u64 v = 0;
+            if (valid) {
+                const u64 slot = S.rs[q] + (k - opi);
+                wedge_op<HASH, PASS>(W, __ldg(g.adj + slot), lo, half, slot_acc, slot, v);
+            }
+            if (PASS == 1) {
+                const u32 off = k - opi;
+                const u32 seg0 = lane > off ? lane - off : 0u;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const u64 t = __shfl_up_sync(0xffffffffu, v, d);
+                    if (lane >= seg0 + (u32)d) v += t;
+                }
+                const bool tail = valid && (lane == 31 || k + 1 == ke || (owner < 31 && k + 1 == onx));
+                if (tail && v) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v);
+            }
+            k0 += 32;
+            bs = __shfl_sync(0xffffffffu, q, 31);
+        }
+    }
+}
+
+__host__ __device__ constexpr u32 tab_words(bool hash) { return hash ? kMidSlots + kMidSlots / 2 : (u32)kWindow; }
+__host__ __device__ constexpr int tab_threads(bool hash) { return hash ? kMidThreads : kBigThreads; }
+
+// Mid and big tops: one block per top a (persistent blocks, atomic queue over
+// the cost-sorted list).  Big tops (!HASH) sweep c in dense shared-memory
+// windows (16-bit packed counters while |L(a)| < 65536: 2*kWindow c-values
+// per window, else 32-bit: kWindow); per window the non-empty runs
+// N(b) n [lo,hi) of the lower neighbours b are found by galloping from each
+// b's cursor, compacted (flag scan) and prefix-summed in per-block global
+// scratch, then walked by window_pass.  Mid tops (HASH, <= kMidWedges wedges)
+// take all c < a at once in a block hash: runs are the full row prefixes
+// N(b) n [0,a), one "window", no cursors.  Credits go to per-adjacency-slot
+// accumulators (consecutive wedges of a run are consecutive slots), folded
+// into edge rows by k_fold_slots.
+template <bool HASH>
+__global__ void __launch_bounds__(tab_threads(HASH), HASH ? 2 : 1)
+k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
+              i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
+    constexpr int THREADS = tab_threads(HASH);
+    constexpr u32 kWords = tab_words(HASH);
+    extern __shared__ u32 W[]; // kWords words
     __shared__ unsigned long long s_idx;
     __shared__ u32 s_next;
-    const u32 lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const u32 wid = threadIdx.x >> 5, nwarps = THREADS / 32;
     BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
-    for (u32 i = threadIdx.x; i < kWindow; i += blockDim.x) W[i] = 0;
+    for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
@@ -588,157 +751,75 @@ k_cycle_big(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lon
         const u64 E0 = g.loff[a];
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
-        const bool half = nb < 65536u;
+        const bool half = HASH || nb < 65536u;
         const u32 span = half ? 2u * kWindow : (u32)kWindow;
-        if (threadIdx.x == 0) s_next = kEmpty;
+        if (threadIdx.x == 0) s_next = HASH ? 0u : kEmpty;
         __syncthreads();
-        for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
-            S.cur[j] = 0;
+        // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at 0
+        for (u32 j = threadIdx.x; j < nb; j += THREADS) {
             const u64 e = E0 + j;
-            if (g.epos[e] > 0) atomicMin(&s_next, g.adj[g.off[g.eu[e]]]);
+            const u64 rb = g.off[g.eu[e]];
+            const u32 re = g.epos[e];
+            S.rb[j] = rb;
+            S.rend[j] = re;
+            S.cur[j] = 0;
+            if (!HASH && re > 0) atomicMin(&s_next, g.adj[rb]);
         }
         __syncthreads();
         u32 lo = s_next;
         while (lo != kEmpty && lo < a) {
-            const u32 hi = (u64)lo + span < (u64)a ? lo + span : a;
+            const u32 hi = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a);
             // runs [cur, hpos) of every b; flag non-empty ones
-            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
-                const u64 e = E0 + j;
-                const u64 rb = g.off[g.eu[e]];
+            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
                 const u32 c0 = S.cur[j];
-                const u64 p = gallop_lower_bound(g.adj, rb + c0, rb + g.epos[e], hi);
-                S.hpos[j] = (u32)(p - rb);
-                S.pre[j] = p - rb > c0 ? 1u : 0u;
+                const u64 rb = S.rb[j];
+                const u32 h = HASH ? S.rend[j] : (u32)(gallop_lower_bound(g.adj, rb + c0, rb + S.rend[j], hi) - rb);
+                S.hpos[j] = h;
+                S.pre[j] = h > c0 ? 1u : 0u;
             }
             __syncthreads();
-            const u32 nnz = block_exclusive_scan<kBigThreads>(S.pre, nb);
+            const u32 nnz = block_exclusive_scan<THREADS>(S.pre, nb);
             // compact: run j -> position pre[j]; hpos still holds the run ends
-            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
+            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
                 const u32 c0 = S.cur[j], h = S.hpos[j];
                 if (h > c0) {
                     const u32 q = S.pre[j];
                     S.rj[q] = j;
-                    S.rs[q] = g.off[g.eu[E0 + j]] + c0;
+                    S.rs[q] = S.rb[j] + c0;
                 }
             }
             __syncthreads();
             // run lengths in compacted order, then their prefix (reusing pre)
-            for (u32 q = threadIdx.x; q < nnz; q += blockDim.x) {
+            for (u32 q = threadIdx.x; q < nnz; q += THREADS) {
                 const u32 j = S.rj[q];
                 S.pre[q] = S.hpos[j] - S.cur[j];
             }
             __syncthreads();
-            const u32 T = block_exclusive_scan<kBigThreads>(S.pre, nnz);
+            const u32 T = block_exclusive_scan<THREADS>(S.pre, nnz);
             if (threadIdx.x == 0) S.pre[nnz] = T;
             __syncthreads();
-            const bool bulk_clear = T > (u32)(kWindow / 8);
-            // each warp walks a contiguous range of wedges: one binary search
-            // per pass, then the run pointer advances by ballot
+            const bool bulk_clear = HASH || T > kWords / 8;
             const u32 per = ((T + nwarps * 32 - 1) / (nwarps * 32)) * 32;
-            const u32 kb = wid * per, ke = kb + per < T ? kb + per : T;
-            for (int pass = 0; pass < (bulk_clear ? 2 : 3); ++pass) {
-                if (kb < ke) {
-                    // round state: run pointer bs, the 32 run starts pi, each
-                    // lane's run q, slot and neighbour id cv.  The next round's
-                    // mapping and adjacency load are issued before this
-                    // round's atomics (software pipelining).
-                    u32 bs = upper_bound_dev<u32, u32>(S.pre, 0, nnz + 1, kb) - 1; // warp-uniform
-                    u32 k0 = kb;
-                    u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
-                    u32 q;
-                    u64 slot = 0;
-                    u32 cv = 0;
-                    {
-                        const u32 k = k0 + lane;
-                        u32 owner = 0;
-#pragma unroll
-                        for (int step = 16; step > 0; step >>= 1) {
-                            const u32 cand = owner + step;
-                            const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
-                            if (cand < 32 && ex <= k) owner = cand;
-                        }
-                        q = bs + owner;
-                        const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
-                        if (k < ke) {
-                            slot = S.rs[q] + (k - opi);
-                            cv = g.adj[slot];
-                        }
-                    }
-                    for (;;) {
-                        const u32 kn = k0 + 32;
-                        const bool more = kn < ke;
-                        u32 n_bs = bs, n_pi = pi, n_q = 0, n_cv = 0;
-                        u64 n_slot = 0;
-                        if (more) {
-                            unsigned bal = __ballot_sync(0xffffffffu, pi <= kn);
-                            while (bal == 0xffffffffu) {
-                                n_bs += 31;
-                                n_pi = n_bs + lane <= nnz ? S.pre[n_bs + lane] : 0xffffffffu;
-                                bal = __ballot_sync(0xffffffffu, n_pi <= kn);
-                            }
-                            n_bs += 31 - __clz(bal);
-                            n_pi = n_bs + lane <= nnz ? S.pre[n_bs + lane] : 0xffffffffu;
-                            const u32 k = kn + lane;
-                            u32 owner = 0;
-#pragma unroll
-                            for (int step = 16; step > 0; step >>= 1) {
-                                const u32 cand = owner + step;
-                                const u32 ex = __shfl_sync(0xffffffffu, n_pi, cand & 31);
-                                if (cand < 32 && ex <= k) owner = cand;
-                            }
-                            n_q = n_bs + owner;
-                            const u32 opi = __shfl_sync(0xffffffffu, n_pi, owner);
-                            if (k < ke) {
-                                n_slot = S.rs[n_q] + (k - opi);
-                                n_cv = g.adj[n_slot];
-                            }
-                        }
-                        // process this round
-                        const bool valid = k0 + lane < ke;
-                        u64 key = ~0ull, val = 0;
-                        if (valid) {
-                            const u32 ci = cv - lo;
-                            if (pass == 0) {
-                                w_inc(W, ci, half);
-                            } else if (pass == 1) {
-                                val = w_get(W, ci, half) - 1;
-                                key = q;
-                                if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
-                            } else {
-                                if (half)
-                                    W[ci >> 1] = 0;
-                                else
-                                    W[ci] = 0;
-                            }
-                        }
-                        if (pass == 1) {
-                            u64 sum;
-                            const bool tail = seg_tail_sum(key, val, &sum);
-                            if (valid && tail && sum) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)sum);
-                        }
-                        if (!more) break;
-                        k0 = kn;
-                        bs = n_bs;
-                        pi = n_pi;
-                        q = n_q;
-                        slot = n_slot;
-                        cv = n_cv;
-                    }
-                }
-                __syncthreads();
-            }
+            const u32 kb = wid * per < T ? wid * per : T;
+            const u32 ke = kb + per < T ? kb + per : T;
+            window_pass<HASH, 0>(g, S, nnz, kb, ke, W, lo, half, abase, slot_acc);
+            __syncthreads();
+            window_pass<HASH, 1>(g, S, nnz, kb, ke, W, lo, half, abase, slot_acc);
+            __syncthreads();
             if (bulk_clear) {
-                const u32 words = half ? (hi - lo + 1) >> 1 : hi - lo;
-                for (u32 i = threadIdx.x; i < words; i += blockDim.x) W[i] = 0;
+                const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
+                for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
+            } else if (!HASH) {
+                window_pass<HASH, 2>(g, S, nnz, kb, ke, W, lo, half, abase, slot_acc);
             }
+            if (HASH) break;
             // advance cursors, next non-empty window start
             if (threadIdx.x == 0) s_next = kEmpty;
             __syncthreads();
-            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) {
+            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
                 const u32 h = S.hpos[j];
                 S.cur[j] = h;
-                const u64 e = E0 + j;
-                if (h < g.epos[e]) atomicMin(&s_next, g.adj[g.off[g.eu[e]] + h]);
+                if (h < S.rend[j]) atomicMin(&s_next, g.adj[S.rb[j] + h]);
             }
             __syncthreads();
             lo = s_next;
@@ -883,19 +964,25 @@ __global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* 
     if (ls) atomicAdd(&cnt[1], ls);
 }
 
+// cycle work list key = wedges of top a; classes big (> kMidWedges, dense
+// windows), mid (> kSmallWedges, block hash), small (warp hash)
 __global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u64* __restrict__ keys,
-                           unsigned long long* __restrict__ cnt) {
-    unsigned long long lb = 0, ls = 0;
+                           unsigned long long* __restrict__ n_big, unsigned long long* __restrict__ n_mid,
+                           unsigned long long* __restrict__ n_small) {
+    unsigned long long lb = 0, lm = 0, ls = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         u64 w = wpre[g.loff[a + 1]] - wpre[g.loff[a]];
         keys[a] = w;
-        if (w > kSmallWedges)
+        if (w > kMidWedges)
             ++lb;
+        else if (w > kSmallWedges)
+            ++lm;
         else if (w)
             ++ls;
     }
-    if (lb) atomicAdd(&cnt[0], lb);
-    if (ls) atomicAdd(&cnt[1], ls);
+    if (lb) atomicAdd(n_big, lb);
+    if (lm) atomicAdd(n_mid, lm);
+    if (ls) atomicAdd(n_small, ls);
 }
 
 // rank's share of a cost-sorted list: sorted positions p with p % world == rank
@@ -1068,33 +1155,51 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u64* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
-            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.wpre.as<u64>(), kin, counters + 10);
+            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,
+                                                           counters + 11);
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
             const u64 nbig = read_dev<unsigned long long>(counters + 10, s);
+            const u64 nmid = read_dev<unsigned long long>(counters + 15, s);
             const u64 nsmall = read_dev<unsigned long long>(counters + 11, s);
             cs.work[2] = 12 * read_dev(cs.wpre.as<u64>() + m, s) / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
             const u64 mybig = rank_share(nbig, rank, world);
+            const u64 mymid = rank_share(nmid, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
             u32* lbig = iin;
-            u32* lsmall = iin + mybig;
-            if (mybig) {
-                k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
-                GL_LAUNCH_CHECK();
-                u32 cap = g.dmax + 2;
-                const unsigned blocks = (unsigned)sms;
+            u32* lmid = iin + mybig;
+            u32* lsmall = lmid + mymid;
+            if (mybig || mymid) {
+                const u32 cap = (g.dmax + 3) & ~1u;
+                const unsigned blocks = (unsigned)sms * 2; // 1 big or 2 mid blocks per SM
                 cs.cursor.alloc((u64)blocks * ((big_scratch_words(cap) + 1) & ~1ull) * sizeof(u32));
-                const size_t smem = (size_t)kWindow * sizeof(u32);
-                GL_CUDA(cudaFuncSetAttribute(k_cycle_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_cycle_big<<<blocks, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1, cs.slots.as<i64>(),
-                                                              cs.cursor.as<u32>(), cap);
-                GL_LAUNCH_CHECK();
-                cs.launches += 2;
+                if (mybig) {
+                    k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
+                    GL_LAUNCH_CHECK();
+                    const size_t smem = (size_t)tab_words(false) * sizeof(u32);
+                    GL_CUDA(cudaFuncSetAttribute(k_cycle_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+                    k_cycle_block<false><<<(unsigned)sms, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1,
+                                                                          cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
+                    GL_LAUNCH_CHECK();
+                    cs.launches += 2;
+                }
+                if (mymid) {
+                    k_take_rank<<<grid1d(mymid, 256, sms), 256, 0, s>>>(iout, nbig, nmid, rank, world, lmid);
+                    GL_LAUNCH_CHECK();
+                    const size_t smem = (size_t)tab_words(true) * sizeof(u32);
+                    GL_CUDA(cudaFuncSetAttribute(k_cycle_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+                    k_cycle_block<true><<<blocks, kMidThreads, smem, s>>>(g, lmid, mymid, counters + 4,
+                                                                         cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
+                    GL_LAUNCH_CHECK();
+                    cs.launches += 2;
+                }
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig, nsmall, rank, world, lsmall);
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmid, nsmall, rank, world, lsmall);
                 GL_LAUNCH_CHECK();
                 const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_cycle_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -158,6 +158,35 @@ def test_big_top_windows(cuda_device):
     assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
 
 
+def test_multiwindow_half_counters(cuda_device):
+    """n > 65536: big tops span several 64K-id windows of 16-bit counters."""
+    pairs = gl.generate_ba(200000, 4, seed=11)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert g.num_vertices() > 65536
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
+def test_hub_full_counters(cuda_device):
+    """A hub with |L(a)| >= 65536 switches k_cycle_big to 32-bit counters
+    (32K-id windows); leaves carry a sparse random graph plus a second hub so
+    the hub's wedges close 4-cycles through many windows."""
+    rng = np.random.default_rng(7)
+    leaves = 70000
+    hub = [(0, i) for i in range(1, leaves + 1)]
+    hub2 = [(leaves + 1, int(i)) for i in rng.choice(np.arange(1, leaves + 1), 3000, replace=False)]
+    ab = rng.integers(1, leaves + 1, size=(20000, 2))
+    pairs = np.array(hub + hub2 + [tuple(map(int, r)) for r in ab], dtype=np.uint64)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert g.max_degree() >= 65536
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
 def test_sharded_equals_single(cuda_device):
     """world=2 sharding emulated on one GPU: begin per rank, sum partial rows,
     finish per shard, sum unrestricted -> identical macro and micro."""

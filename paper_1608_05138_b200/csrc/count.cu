@@ -43,10 +43,11 @@ constexpr int kCycleSmallWarps = 8;  // warps per small-top block
 constexpr int kHashSlots = 1024;     // per-warp hash slots (small tops)
 constexpr u64 kSmallWedges = 512;    // small-top threshold (<= half the slots)
 constexpr int kBigThreads = 1024;    // block per big top (dense windows), one block per SM
-constexpr int kMidThreads = 512;     // block per mid top (hash), two blocks per SM
+constexpr int kMidThreads = 1024;    // block per mid top (hash), one block per SM
 constexpr int kWindow = 32768;       // dense W window words (u32, or 2 x u16) in shared memory
-constexpr u32 kMidSlots = 16384;     // mid tops: block hash, u32 keys + u16 counts (96 KB)
-constexpr u64 kMidWedges = 8192;     // mid-top threshold (<= half the hash slots)
+constexpr int kMidLog = 15;
+constexpr u32 kMidSlots = 1u << kMidLog; // mid tops: block hash, u32 keys + u16 counts (192 KB)
+constexpr u64 kMidWedges = kMidSlots / 2; // mid-top threshold (<= half the hash slots)
 
 constexpr u32 kEmpty = 0xffffffffu;
 
@@ -558,8 +559,14 @@ __device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64
 
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
-    u32 *cur, *hpos, *rend, *pre, *rj;
-    u64 *rb, *rs;
+    u32 *cur, *hpos, *rend, *pre, *rj, *rs;
+    u64* rb;
+};
+// compacted runs of one window: wedge prefix pre[nnz+1], first adjacency slot
+// rs[q] (u32: 2m < 2^32 is checked on the host), lower-neighbour index rj[q];
+// in shared memory when nnz fits, else in the block's global scratch
+struct RunMeta {
+    u32 *pre, *rs, *rj;
 };
 __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     BigScratch s;
@@ -568,18 +575,16 @@ __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     s.rend = base + 2 * (u64)cap;
     s.pre = base + 3 * (u64)cap;              // cap + 1 entries
     s.rj = base + 4 * (u64)cap + 1;
-    u64* q = reinterpret_cast<u64*>(base + ((5 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
-    s.rb = q;
-    s.rs = q + cap;
+    s.rs = base + 5 * (u64)cap + 1;
+    s.rb = reinterpret_cast<u64*>(base + ((6 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
     return s;
 }
-__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 9ull * cap + 8; }
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 8ull * cap + 8; }
 
 // W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
 // or an open-addressing hash over all c < a (mid tops, HASH).  Hash keys are
 // u32 (kEmpty = free), counts u16 packed two per word.
-__device__ __forceinline__ u32 mid_slot(u32 c) { return (c * 0x9E3779B1u) >> (32 - 14); }
-static_assert(kMidSlots == 16384, "mid_slot assumes 16384 slots");
+__device__ __forceinline__ u32 mid_slot(u32 c) { return (c * 0x9E3779B1u) >> (32 - kMidLog); }
 
 template <bool HASH>
 __device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, bool half) {
@@ -634,6 +639,24 @@ __device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, bool half, i64*
     }
 }
 
+// Last index in [0, n) with a[idx] <= x (a non-decreasing, a[0] <= x), by the
+// whole warp: 32 probes per step, so log32(n) dependent loads instead of log2(n).
+__device__ __forceinline__ u32 warp_upper_bound(const u32* a, u32 n, u32 x) {
+    const u32 lane = lane_id();
+    u32 lo = 0, hi = n;
+    while (hi - lo > 32u) {
+        const u32 step = (hi - lo + 31u) >> 5;
+        const u32 idx = lo + lane * step;
+        const bool ok = idx < hi && a[idx] <= x;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        lo += (31u - __clz(bal)) * step;
+        hi = lo + step < hi ? lo + step : hi;
+    }
+    const u32 idx = lo + lane;
+    const unsigned bal = __ballot_sync(0xffffffffu, idx < hi && a[idx] <= x);
+    return lo + 31u - __clz(bal);
+}
+
 // One pass over a warp's range [kb, ke) of a window's flattened wedge list
 // (compacted runs q, S.pre = wedge prefix, run q = adjacency slots
 // [S.rs[q], S.rs[q] + len)).  Stretches of full 32-wedge rounds inside one
@@ -644,12 +667,14 @@ __device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, bool half, i64*
 // a segmented shuffle sum whose tail lanes issue the RED.
 //   PASS 0: W[c]++     PASS 1: credit W[c]-1 to (b,c) and, summed, to (a,b)
 //   PASS 2: W[c] = 0 (sparse clear of a dense window)
+constexpr int kUnroll = 8; // uniform-path rounds with loads in flight per lane
+
 template <bool HASH, int PASS>
-__device__ __forceinline__ void window_pass(const DevGraph& g, const BigScratch& S, u32 nnz, u32 kb, u32 ke, u32* W,
+__device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,
                                             u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
     const u32 lane = lane_id();
     if (kb >= ke) return;
-    u32 bs = upper_bound_dev<u32, u32>(S.pre, 0, nnz + 1, kb) - 1; // warp-uniform
+    u32 bs = warp_upper_bound(S.pre, nnz + 1, kb);
     u32 k0 = kb;
     while (k0 < ke) {
         u32 e1 = S.pre[bs + 1];
@@ -658,14 +683,14 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const BigScratch&
         if (stop - k0 >= 32u) {
             // uniform stretch of full rounds inside run bs
             const u32 nfull = (stop - k0) >> 5;
-            const u64 sbase = S.rs[bs] + (k0 - S.pre[bs]) + lane;
+            const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
             u64 acc = 0;
-            for (u32 r = 0; r < nfull; r += 4) {
-                u32 cv[4];
+            for (u32 r = 0; r < nfull; r += kUnroll) {
+                u32 cv[kUnroll];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) cv[u] = r + u < nfull ? __ldg(g.adj + sbase + 32u * (r + u)) : kEmpty;
+                for (int u = 0; u < kUnroll; ++u) cv[u] = r + u < nfull ? __ldg(g.adj + sbase + 32u * (r + u)) : kEmpty;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kUnroll; ++u) {
                     if (cv[u] != kEmpty) {
                         u64 v = 0;
                         wedge_op<HASH, PASS>(W, cv[u], lo, half, slot_acc, sbase + 32u * (r + u), v);
@@ -695,7 +720,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const BigScratch&
             const u32 q = bs + owner;
             u64 v = 0;
             if (valid) {
-                const u64 slot = S.rs[q] + (k - opi);
+                const u64 slot = (u64)S.rs[q] + (k - opi);
                 wedge_op<HASH, PASS>(W, __ldg(g.adj + slot), lo, half, slot_acc, slot, v);
             }
             if (PASS == 1) {
@@ -717,29 +742,53 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const BigScratch&
 
 __host__ __device__ constexpr u32 tab_words(bool hash) { return hash ? kMidSlots + kMidSlots / 2 : (u32)kWindow; }
 __host__ __device__ constexpr int tab_threads(bool hash) { return hash ? kMidThreads : kBigThreads; }
+// runs whose metadata fits in shared memory beside the table (12 B per run)
+__host__ __device__ constexpr u32 meta_cap(bool hash) { return hash ? 2048u : 7168u; }
+__host__ __device__ constexpr u32 smem_words(bool hash) { return tab_words(hash) + 3 * meta_cap(hash) + 1; }
+// wedges per dynamic work grab of one warp: ~8 grabs per warp and pass, at least 512
+__device__ __forceinline__ u32 grab_size(u32 T, u32 nwarps) {
+    const u32 g = (T / (nwarps * 8u) + 31u) & ~31u;
+    return g > 512u ? g : 512u;
+}
 
 // Mid and big tops: one block per top a (persistent blocks, atomic queue over
 // the cost-sorted list).  Big tops (!HASH) sweep c in dense shared-memory
 // windows (16-bit packed counters while |L(a)| < 65536: 2*kWindow c-values
 // per window, else 32-bit: kWindow); per window the non-empty runs
 // N(b) n [lo,hi) of the lower neighbours b are found by galloping from each
-// b's cursor, compacted (flag scan) and prefix-summed in per-block global
-// scratch, then walked by window_pass.  Mid tops (HASH, <= kMidWedges wedges)
-// take all c < a at once in a block hash: runs are the full row prefixes
-// N(b) n [0,a), one "window", no cursors.  Credits go to per-adjacency-slot
-// accumulators (consecutive wedges of a run are consecutive slots), folded
-// into edge rows by k_fold_slots.
+// b's cursor, compacted (flag scan) and prefix-summed -- in shared memory when
+// they fit (RunMeta) -- and walked by window_pass, warps grabbing kGrab-wedge
+// ranges from a shared counter so that the cost differences between long-run
+// and short-run ranges do not stall the block at the pass barriers.  Mid tops
+// (HASH, <= kMidWedges wedges) take all c < a at once in a block hash: runs
+// are the full row prefixes N(b) n [0,a), one "window", no cursors.  Credits
+// go to per-adjacency-slot accumulators (consecutive wedges of a run are
+// consecutive slots), folded into edge rows by k_fold_slots.
+template <bool HASH, int PASS>
+__device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u32 nnz, u32 T, u32* counter, u32* W,
+                                          u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
+    const u32 grab = grab_size(T, blockDim.x >> 5);
+    for (;;) {
+        u32 k0 = 0;
+        if (lane_id() == 0) k0 = atomicAdd(counter, grab);
+        k0 = __shfl_sync(0xffffffffu, k0, 0);
+        if (k0 >= T) break;
+        window_pass<HASH, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, half, abase, slot_acc);
+    }
+}
+
 template <bool HASH>
-__global__ void __launch_bounds__(tab_threads(HASH), HASH ? 2 : 1)
+__global__ void __launch_bounds__(tab_threads(HASH), 1)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
     constexpr int THREADS = tab_threads(HASH);
     constexpr u32 kWords = tab_words(HASH);
-    extern __shared__ u32 W[]; // kWords words
+    extern __shared__ u32 W[]; // kWords table words, then the run metadata
     __shared__ unsigned long long s_idx;
-    __shared__ u32 s_next;
-    const u32 wid = threadIdx.x >> 5, nwarps = THREADS / 32;
+    __shared__ u32 s_next, s_work[3];
     BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
+    const RunMeta Msm{W + kWords, W + kWords + meta_cap(HASH) + 1, W + kWords + 2 * meta_cap(HASH) + 1};
+    const RunMeta Mgl{S.pre, S.rs, S.rj};
     for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
     for (;;) {
         __syncthreads();
@@ -779,38 +828,38 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             }
             __syncthreads();
             const u32 nnz = block_exclusive_scan<THREADS>(S.pre, nb);
-            // compact: run j -> position pre[j]; hpos still holds the run ends
+            const RunMeta M = nnz <= meta_cap(HASH) ? Msm : Mgl;
+            // compact: run j -> position pre[j] (global flags; M.pre is
+            // rewritten only after the compaction barrier)
             for (u32 j = threadIdx.x; j < nb; j += THREADS) {
                 const u32 c0 = S.cur[j], h = S.hpos[j];
                 if (h > c0) {
                     const u32 q = S.pre[j];
-                    S.rj[q] = j;
-                    S.rs[q] = S.rb[j] + c0;
+                    M.rj[q] = j;
+                    M.rs[q] = (u32)(S.rb[j] + c0);
                 }
             }
             __syncthreads();
-            // run lengths in compacted order, then their prefix (reusing pre)
+            // run lengths in compacted order, then their prefix
             for (u32 q = threadIdx.x; q < nnz; q += THREADS) {
-                const u32 j = S.rj[q];
-                S.pre[q] = S.hpos[j] - S.cur[j];
+                const u32 j = M.rj[q];
+                M.pre[q] = S.hpos[j] - S.cur[j];
             }
+            if (threadIdx.x < 3) s_work[threadIdx.x] = 0;
             __syncthreads();
-            const u32 T = block_exclusive_scan<THREADS>(S.pre, nnz);
-            if (threadIdx.x == 0) S.pre[nnz] = T;
+            const u32 T = block_exclusive_scan<THREADS>(M.pre, nnz);
+            if (threadIdx.x == 0) M.pre[nnz] = T;
             __syncthreads();
             const bool bulk_clear = HASH || T > kWords / 8;
-            const u32 per = ((T + nwarps * 32 - 1) / (nwarps * 32)) * 32;
-            const u32 kb = wid * per < T ? wid * per : T;
-            const u32 ke = kb + per < T ? kb + per : T;
-            window_pass<HASH, 0>(g, S, nnz, kb, ke, W, lo, half, abase, slot_acc);
+            grab_pass<HASH, 0>(g, M, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
             __syncthreads();
-            window_pass<HASH, 1>(g, S, nnz, kb, ke, W, lo, half, abase, slot_acc);
+            grab_pass<HASH, 1>(g, M, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
             __syncthreads();
             if (bulk_clear) {
                 const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
                 for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
             } else if (!HASH) {
-                window_pass<HASH, 2>(g, S, nnz, kb, ke, W, lo, half, abase, slot_acc);
+                grab_pass<HASH, 2>(g, M, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
             }
             if (HASH) break;
             // advance cursors, next non-empty window start
@@ -1172,13 +1221,14 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* lmid = iin + mybig;
             u32* lsmall = lmid + mymid;
             if (mybig || mymid) {
+                if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
                 const u32 cap = (g.dmax + 3) & ~1u;
                 const unsigned blocks = (unsigned)sms * 2; // 1 big or 2 mid blocks per SM
                 cs.cursor.alloc((u64)blocks * ((big_scratch_words(cap) + 1) & ~1ull) * sizeof(u32));
                 if (mybig) {
                     k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
                     GL_LAUNCH_CHECK();
-                    const size_t smem = (size_t)tab_words(false) * sizeof(u32);
+                    const size_t smem = (size_t)smem_words(false) * sizeof(u32);
                     GL_CUDA(cudaFuncSetAttribute(k_cycle_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
                     k_cycle_block<false><<<(unsigned)sms, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1,
@@ -1189,10 +1239,10 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 if (mymid) {
                     k_take_rank<<<grid1d(mymid, 256, sms), 256, 0, s>>>(iout, nbig, nmid, rank, world, lmid);
                     GL_LAUNCH_CHECK();
-                    const size_t smem = (size_t)tab_words(true) * sizeof(u32);
+                    const size_t smem = (size_t)smem_words(true) * sizeof(u32);
                     GL_CUDA(cudaFuncSetAttribute(k_cycle_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
-                    k_cycle_block<true><<<blocks, kMidThreads, smem, s>>>(g, lmid, mymid, counters + 4,
+                    k_cycle_block<true><<<(unsigned)sms, kMidThreads, smem, s>>>(g, lmid, mymid, counters + 4,
                                                                          cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;

@@ -38,6 +38,12 @@ def main(rep, top=30):
         tot_s += s
         tot_i += i
     print(f'# {rep}: {tot_s} samples, {tot_i:.3e} warp instructions')
+    allst = defaultdict(int)
+    for v in agg.values():
+        for k, c in v[3].items():
+            allst[k] += c
+    tot = max(1, sum(allst.values()))
+    print('# stall mix: ' + ', '.join(f'{k}={100 * c / tot:.1f}%' for k, c in sorted(allst.items(), key=lambda x: -x[1])[:8]))
     for (f, ln), (s, i, src, st) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
         tops = ','.join(f'{k}={v}' for k, v in sorted(st.items(), key=lambda x: -x[1])[:3])
         print(f'{100 * s / max(1, tot_s):5.1f}% {100 * i / max(1, tot_i):5.1f}%i {f}:{ln:<5} {src:<60} {tops}')

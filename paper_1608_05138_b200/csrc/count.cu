@@ -37,8 +37,6 @@ namespace gl {
 
 namespace {
 
-constexpr int kTriThreads = 256;
-constexpr int kTriTile = 2048;       // probes per block tile
 constexpr int kCycleSmallWarps = 8;  // warps per small-top block
 constexpr int kHashSlots = 1024;     // per-warp hash slots (small tops)
 constexpr u64 kSmallWedges = 512;    // small-top threshold (<= half the slots)
@@ -66,124 +64,39 @@ inline unsigned grid1d(u64 n, int threads, int sms, int per_sm = 8) {
     return (unsigned)g;
 }
 
-__device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
-}
 
 // ------------------------------------------------------------------ prepass
 
-// probes(e) = min(|U(u) after v|, |U(v)|), wedges(e) = epos(e)
-// lsum (optional): sum of |A|+|B| over edges with probes, i.e. the adjacency
-// entries a merge-based intersection would read (the algorithmic bytes / 4).
-__global__ void k_prepass(DevGraph g, u64* __restrict__ probes, u64* __restrict__ wedges,
-                          unsigned long long* __restrict__ lsum) {
-    u64 acc = 0;
-    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < g.m; e += (u64)gridDim.x * blockDim.x) {
-        u32 v = g.ev[e], u = g.eu[e];
-        u64 la = g.off[u + 1] - (g.off[u] + g.epos[e] + 1);
-        u64 lb = g.off[v + 1] - (g.off[v] + g.lcnt[v]);
-        bool any = la && lb;
-        probes[e] = any ? (la < lb ? la : lb) : 0;
+// wedges(e) = epos(e): the wedges a-b-c (c < a) of edge e = (a,b) as top edge
+__global__ void k_prepass(DevGraph g, u64* __restrict__ wedges) {
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < g.m; e += (u64)gridDim.x * blockDim.x)
         wedges[e] = g.epos[e];
-        acc += any ? la + lb : 0;
-    }
-    if (lsum) {
-        for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-        if ((threadIdx.x & 31) == 0 && acc) atomicAdd(lsum, (unsigned long long)acc);
-    }
 }
 
-// ------------------------------------------------------------------ triangles
-
-struct TriCtx {
-    u32 v, u;
-    u64 a_begin, a_end, b_begin, b_end;
-};
-
-__device__ __forceinline__ TriCtx tri_ctx(const DevGraph& g, u64 e) {
-    TriCtx c;
-    c.v = g.ev[e];
-    c.u = g.eu[e];
-    c.a_begin = g.off[c.u] + g.epos[e] + 1;
-    c.a_end = g.off[c.u + 1];
-    c.b_begin = g.off[c.v] + g.lcnt[c.v];
-    c.b_end = g.off[c.v + 1];
-    return c;
-}
-
-// Probe r of edge e: returns found, and the A-side (u row) / B-side (v row) slots.
-__device__ __forceinline__ bool tri_probe(const DevGraph& g, const TriCtx& c, u64 r, u64* sa, u64* sb) {
-    const u64 la = c.a_end - c.a_begin, lb = c.b_end - c.b_begin;
-    if (la <= lb) {
-        u64 s = c.a_begin + r;
-        u32 x = g.adj[s];
-        u64 p = lower_bound_dev<u32, u64>(g.adj, c.b_begin, c.b_end, x);
-        *sa = s;
-        *sb = p;
-        return p < c.b_end && g.adj[p] == x;
-    } else {
-        u64 s = c.b_begin + r;
-        u32 x = g.adj[s];
-        u64 p = lower_bound_dev<u32, u64>(g.adj, c.a_begin, c.a_end, x);
-        *sa = p;
-        *sb = s;
-        return p < c.a_end && g.adj[p] == x;
-    }
-}
-
-// S(e) contributions: for every triangle (u < v < c) found at its lowest pair
-// e = (v,u) by one probe of the shorter list, credit -(t of the other two
-// edges) into the y rows of all three edges (y = C4 - S).
-__global__ void __launch_bounds__(kTriThreads)
-k_trisum(DevGraph g, const u64* __restrict__ pre, u64 item_begin, u64 item_end, const u32* __restrict__ t,
-         i64* __restrict__ part) {
-    __shared__ u64 s_e[2];
-    for (u64 tile = item_begin + (u64)blockIdx.x * kTriTile; tile < item_end;
-         tile += (u64)gridDim.x * kTriTile) {
-        const u64 tile_end = tile + kTriTile < item_end ? tile + kTriTile : item_end;
-        __syncthreads();
-        if (threadIdx.x < 2) {
-            u64 x = threadIdx.x == 0 ? tile : tile_end - 1;
-            s_e[threadIdx.x] = upper_bound_dev<u64, u64>(pre, 0, g.m + 1, x) - 1;
-        }
-        __syncthreads();
-        const u64 e_lo = s_e[0], e_end = s_e[1] + 1;
-        for (u64 base = tile; base < tile_end; base += kTriThreads) {
-            const u64 i = base + threadIdx.x;
-            const bool valid = i < tile_end;
-            u64 e = ~0ull;
-            u64 contrib = 0;
-            if (valid) {
-                e = upper_bound_dev<u64, u64>(pre, e_lo, e_end, i) - 1;
-                TriCtx c = tri_ctx(g, e);
-                u64 sa = 0, sb = 0;
-                if (tri_probe(g, c, i - pre[e], &sa, &sb)) {
-                    u32 ea = g.eid[sa], eb = g.eid[sb];
-                    u64 te = t[e], ta = t[ea], tb = t[eb];
-                    atomic_add_i64(&part[2 * (u64)ea + 1], -(i64)(te + tb));
-                    atomic_add_i64(&part[2 * (u64)eb + 1], -(i64)(te + ta));
-                    contrib = ta + tb;
-                }
-            }
-            u64 sum;
-            bool tail = seg_tail_sum(e, contrib, &sum);
-            if (valid && tail && sum) atomic_add_i64(&part[2 * e + 1], -(i64)sum);
-        }
-    }
-}
-
-// ------------------------------------------------------------------ cliques
+// ------------------------------------------------------------------ H-pass
 //
-// Per lowest vertex a, the out-neighbourhood H_a = G[U(a)] is staged as a
-// bitmap adjacency matrix (ceil(k/32) u32 words per row, k = |U(a)|).  Every
-// triangle (a < x < y) is an edge (x,y) of H_a and every 4-clique
-// (a < x < y < z) a triangle of H_a, so one pass over all a yields, each
-// exactly once:
+// Per lowest vertex a, the out-neighbourhood H_a = G[U(a)] (k = |U(a)|
+// members x_0 < ... < x_{k-1}, ascending id).  Every triangle (a < x < y) is
+// an edge (x,y) of H_a and every 4-clique (a < x < y < z) a triangle of H_a.
+//
+// MODE kHPassCount (t and x7 partials), one pass over all a yields, each once:
 //   t(x,y)  += 1                       t(a,x)  += deg_H(x)
 //   x7(x,y) += |N_H(x) n N_H(y)|       x7(a,x) += #triangles of H_a at x
-// Global atomics are per triangle, never per 4-clique (a 4-clique is only
+// with H_a staged as a bitmap adjacency matrix (ceil(k/32) u32 words per row):
+// global atomics are per triangle, never per 4-clique (a 4-clique is only
 // ever a popcount of an AND of two shared-memory rows).
+//
+// MODE kHPassSums (S partials, t complete): every triangle tau = (a,x,y)
+// credits y(e) -= t of the other two edges to each of its three edges
+// (y = C4 - S, S(e) = sum over triangles at e of the other two t's); the
+// (a,x) credits are summed per member in shared memory.
+//
+// H-edges are found by streaming: member x_i's upper list U(x_i) is read
+// coalesced by one warp and every entry is looked up in a shared-memory hash
+// of U(a) (4k slots, u32 keys, u16 member index).  Cost: sum_i |U(x_i)|
+// coalesced adjacency reads + one smem probe each, no global binary search.
 
+constexpr int kHPassCount = 0, kHPassSums = 1;
 constexpr int kHWarpMax = 32;       // 2 <= k <= 32: one warp, one u32 row per lane
 constexpr int kHWarpsPerBlock = 8;
 constexpr int kHBlockThreads = 512; // k > 32: one block per vertex
@@ -191,14 +104,40 @@ constexpr int kHSmemMax = 768;      // k <= 768: workspace in shared memory
 
 __device__ __forceinline__ u64 u_begin(const DevGraph& g, u32 x) { return g.off[x] + g.lcnt[x]; }
 
+constexpr u32 kBloomLog = 16, kBloomWords = (1u << kBloomLog) / 32; // 8 KB member filter
+__device__ __forceinline__ u32 bloom_bit(u32 y) { return (y * 0x2545F491u) >> (32 - kBloomLog); }
+
+__device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 4k, >= 128
+    u32 l = 32 - __clz(4 * k - 1);
+    return l < 7 ? 7 : l;
+}
+__host__ __device__ inline u64 hpass_ws_words(u32 k) {
+    u32 l = 7;
+    while ((1u << l) < 4 * k) ++l;
+    const u64 H = 1ull << l;
+    const u64 W = (k + 31) / 32;
+    const u64 count_ws = 2ull * k + (u64)k * W;  // xs, tri, rows
+    const u64 sums_ws = 4ull * k + 2;            // xs, ta, acc (u64, aligned)
+    return (count_ws > sums_ws ? count_ws : sums_ws) + 2 + H + H / 2 + kBloomWords;
+}
+
+__device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kHWarpsPerBlock * 32)
-k_hclique_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-               u32* __restrict__ t, i64* __restrict__ part) {
+k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
+             u32* __restrict__ t, i64* __restrict__ part) {
     __shared__ u32 s_x[kHWarpsPerBlock][32];
     __shared__ u32 s_row[kHWarpsPerBlock][32];
+    __shared__ u32 s_ta[kHWarpsPerBlock][32];
+    __shared__ unsigned long long s_acc[kHWarpsPerBlock][32];
     const u32 lane = lane_id(), wib = threadIdx.x >> 5;
     u32* xs = s_x[wib];
     u32* rows = s_row[wib];
+    u32* ta = s_ta[wib];
+    unsigned long long* acc = s_acc[wib];
     for (;;) {
         unsigned long long idx = 0;
         if (lane == 0) idx = atomicAdd(queue, 1ull);
@@ -213,8 +152,10 @@ k_hclique_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned 
             x = g.adj[ub + lane];
             xb = u_begin(g, x);
             xe = g.off[x + 1];
+            if (MODE == kHPassSums) ta[lane] = t[g.eid[ub + lane]];
         }
         xs[lane] = x;
+        acc[lane] = 0;
         __syncwarp();
         // phase 1: upper row, bit j > lane set iff x_j in U(x)
         u32 row = 0;
@@ -244,27 +185,40 @@ k_hclique_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned 
         const u32 full = row | col;
         rows[lane] = full;
         __syncwarp();
-        // phase 2: per H-edge common neighbours
+        // phase 2: per H-edge (lane, j > lane)
         u32 tri = 0;
-        u32 bits = full;
+        u32 bits = MODE == kHPassCount ? full : row;
         while (bits) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
-            const u32 c = __popc(full & rows[j]);
-            tri += c;
-            if ((u32)j > lane) {
-                const u32 y = xs[j];
-                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
+            if (MODE == kHPassCount) {
+                const u32 c = __popc(full & rows[j]);
+                tri += c;
+                if ((u32)j > lane) {
+                    const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
+                    const u32 e = g.eid[p];
+                    atomicAdd(&t[e], 1u);
+                    if (c) atomic_add_i64(&part[2 * (u64)e], (i64)c);
+                }
+            } else {
+                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
                 const u32 e = g.eid[p];
-                atomicAdd(&t[e], 1u);
-                if (c) atomic_add_i64(&part[2 * (u64)e], (i64)c);
+                const u64 txy = t[e];
+                atomic_add_i64(&part[2 * (u64)e + 1], -(i64)((u64)ta[lane] + ta[j]));
+                atomicAdd(&acc[lane], (unsigned long long)(ta[j] + txy));
+                atomicAdd(&acc[j], (unsigned long long)(ta[lane] + txy));
             }
         }
+        __syncwarp();
         if (lane < k) {
-            const u32 deg = __popc(full);
             const u32 e = g.eid[ub + lane];
-            if (deg) atomicAdd(&t[e], deg);
-            if (tri) atomic_add_i64(&part[2 * (u64)e], (i64)(tri >> 1));
+            if (MODE == kHPassCount) {
+                const u32 deg = __popc(full);
+                if (deg) atomicAdd(&t[e], deg);
+                if (tri) atomic_add_i64(&part[2 * (u64)e], (i64)(tri >> 1));
+            } else {
+                if (acc[lane]) atomic_add_i64(&part[2 * (u64)e + 1], -(i64)acc[lane]);
+            }
         }
         __syncwarp();
     }
@@ -296,63 +250,26 @@ __device__ u32 block_exclusive_scan(u32* a, u32 n) {
     return s_carry;
 }
 
-// Walk items [kb, ke) of a run-length list with one warp (pre = exclusive
-// prefix over n runs, pre[n] = total): one binary search, then per round of
-// 32 items a 5-step shuffle search for each lane's run and a ballot to
-// advance the run pointer.  f(valid, run, offset) is called converged.
-template <typename F>
-__device__ __forceinline__ void warp_walk(const u32* pre, u32 n, u32 kb, u32 ke, F&& f) {
-    const u32 lane = lane_id();
-    if (kb >= ke) return;
-    u32 bs = upper_bound_dev<u32, u32>(pre, 0, n + 1, kb) - 1;
-    for (u32 k0 = kb; k0 < ke; k0 += 32) {
-        const u32 k = k0 + lane;
-        u32 pi = bs + lane <= n ? pre[bs + lane] : 0xffffffffu;
-        u32 owner = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const u32 cand = owner + step;
-            const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
-            if (cand < 32 && ex <= k) owner = cand;
-        }
-        const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
-        f(k < ke, bs + owner, k - opi);
-        const u32 kn = k0 + 32;
-        if (kn < ke) {
-            unsigned bal = __ballot_sync(0xffffffffu, pi <= kn);
-            while (bal == 0xffffffffu) {
-                bs += 31;
-                pi = bs + lane <= n ? pre[bs + lane] : 0xffffffffu;
-                bal = __ballot_sync(0xffffffffu, pi <= kn);
-            }
-            bs += 31 - __clz(bal);
-        }
-    }
-}
-
-__device__ __forceinline__ u64 hblock_ws_words(u32 k) {
-    return 3ull * k + 1 + (u64)k * ((k + 31) >> 5);
-}
-
-// k > 32: one block per vertex a.  Phase 1 builds H_a's bitmap rows by one
-// probe per (member i, candidate) -- contiguous ranges per warp -- and appends
-// every H-edge (i, j, eid) to a per-block list; phase 2 streams that list:
-// popcount of the two rows, one t and one x7 credit per H-edge; phase 3
-// credits the edges (a, x_i).
+// k > 32: one block per vertex a.  Setup stages U(a) (xs) and its hash;
+// phase 1 streams the members' upper lists (warps grab members), phase 2
+// (kHPassCount) streams the H-edge list: popcount of the two rows, one t and
+// one x7 credit per H-edge; phase 3 credits the edges (a, x_i).
+template <int MODE>
 __global__ void __launch_bounds__(kHBlockThreads)
-k_hclique_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-                u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
-                uint2* __restrict__ hlist_all, u64 hcap) {
+k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
+              u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
+              uint2* __restrict__ hlist_all, u64 hcap) {
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
-    __shared__ u32 s_nh;
-    const u32 lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    uint2* hlist = hlist_all + (u64)blockIdx.x * hcap;
+    __shared__ u32 s_nh, s_mi;
+    const u32 lane = lane_id();
+    uint2* hlist = MODE == kHPassCount ? hlist_all + (u64)blockIdx.x * hcap : nullptr;
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
             s_idx = atomicAdd(queue, 1ull);
             s_nh = 0;
+            s_mi = 0;
         }
         __syncthreads();
         const unsigned long long idx = s_idx;
@@ -361,83 +278,130 @@ k_hclique_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned
         const u64 ub = u_begin(g, a);
         const u32 k = (u32)(g.off[a + 1] - ub);
         const u32 W = (k + 31) >> 5;
+        const u32 hl = hp_log(k), H = 1u << hl;
         u32* ws = k <= (u32)kHSmemMax ? smem : gscratch + (u64)blockIdx.x * gstride;
         u32* xs = ws;
-        u32* pre = xs + k;
-        u32* tri = pre + k + 1;
-        u32* rows = tri + k;
+        u32* tri = xs + k;                      // kHPassCount
+        u32* rows = tri + k;                    // kHPassCount
+        u32* ta = xs + k;                       // kHPassSums
+        unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
+        const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * W : ((2ull * k + 1) & ~1ull) + 2ull * k;
+        u32* bloom = ws + body;
+        u32* hkey = bloom + kBloomWords;
+        unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
         for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-            const u32 x = g.adj[ub + i];
-            xs[i] = x;
-            tri[i] = 0;
-            const u64 lu = g.off[x + 1] - u_begin(g, x);
-            const u32 rem = k - 1 - i;
-            pre[i] = (u32)(lu < rem ? lu : rem);
+            xs[i] = g.adj[ub + i];
+            if (MODE == kHPassCount) {
+                tri[i] = 0;
+            } else {
+                ta[i] = t[g.eid[ub + i]];
+                acc[i] = 0;
+            }
         }
-        for (u64 w = threadIdx.x; w < (u64)k * W; w += blockDim.x) rows[w] = 0;
+        if (MODE == kHPassCount)
+            for (u64 w = threadIdx.x; w < (u64)k * W; w += blockDim.x) rows[w] = 0;
+        for (u32 h = threadIdx.x; h < H; h += blockDim.x) hkey[h] = kEmpty;
+        for (u32 w = threadIdx.x; w < kBloomWords; w += blockDim.x) bloom[w] = 0;
         __syncthreads();
-        const u32 Q = block_exclusive_scan<kHBlockThreads>(pre, k);
-        if (threadIdx.x == 0) pre[k] = Q;
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+            const u32 x = xs[i];
+            u32 h = (x * 0x9E3779B1u) >> (32 - hl);
+            while (atomicCAS(&hkey[h], kEmpty, x) != kEmpty) h = (h + 1) & (H - 1);
+            hval[h] = (unsigned short)i;
+            const u32 bb = bloom_bit(x);
+            atomicOr(&bloom[bb >> 5], 1u << (bb & 31));
+        }
         __syncthreads();
-        // phase 1
-        {
-            const u32 per = ((Q + nwarps * 32 - 1) / (nwarps * 32)) * 32;
-            const u32 kb = wid * per, ke = kb + per < Q ? kb + per : Q;
-            warp_walk(pre, k, kb, ke, [&](bool valid, u32 i, u32 r) {
-                bool found = false;
-                u32 j = 0, e = 0;
-                if (valid) {
-                    const u32 x = xs[i];
-                    const u64 xb = u_begin(g, x), xe = g.off[x + 1];
-                    if (xe - xb <= (u64)(k - 1 - i)) {
-                        const u32 y = g.adj[xb + r];
-                        j = lower_bound_dev<u32, u32>(xs, i + 1, k, y);
-                        found = j < k && xs[j] == y;
-                        if (found) e = g.eid[xb + r];
-                    } else {
-                        j = i + 1 + r;
-                        const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
-                        found = p < xe && g.adj[p] == xs[j];
-                        if (found) e = g.eid[p];
+        const u32 xmax = xs[k - 1];
+        // phase 1: warps grab members i < k-1 and stream U(x_i)
+        for (;;) {
+            u32 i = 0;
+            if (lane == 0) i = atomicAdd(&s_mi, 1u);
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i + 1 >= k) break;
+            const u32 x = xs[i];
+            const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+            for (u64 p0 = xb; p0 < xe; p0 += 128) {
+                u32 yv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const u64 p = p0 + 32u * u + lane;
+                    yv[u] = p < xe ? __ldg(g.adj + p) : kEmpty;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const u64 p = p0 + 32u * u + lane;
+                    const u32 y = yv[u];
+                    bool hit = false;
+                    u32 j = 0;
+                    const u32 bb = bloom_bit(y);
+                    if (y <= xmax && ((bloom[bb >> 5] >> (bb & 31)) & 1u)) { // kEmpty > xmax
+                        u32 h = (y * 0x9E3779B1u) >> (32 - hl);
+                        for (;;) {
+                            const u32 kk = hkey[h];
+                            if (kk == y) {
+                                hit = true;
+                                j = hval[h];
+                                break;
+                            }
+                            if (kk == kEmpty) break;
+                            h = (h + 1) & (H - 1);
+                        }
                     }
-                    if (found) {
-                        atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
-                        atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
+                    u32 e = 0;
+                    if (hit) e = g.eid[p];
+                    if (MODE == kHPassCount) {
+                        if (hit) {
+                            atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
+                            atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
+                        }
+                        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                        if (bal) {
+                            u32 base = 0;
+                            if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
+                            base = __shfl_sync(0xffffffffu, base, 0);
+                            if (hit) hlist[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
+                        }
+                    } else if (hit) {
+                        const u64 txy = t[e];
+                        atomic_add_i64(&part[2 * (u64)e + 1], -(i64)((u64)ta[i] + ta[j]));
+                        atomicAdd(&acc[i], (unsigned long long)(ta[j] + txy));
+                        atomicAdd(&acc[j], (unsigned long long)(ta[i] + txy));
                     }
                 }
-                const unsigned bal = __ballot_sync(0xffffffffu, found);
-                u32 base = 0;
-                if (lane == 0 && bal) base = atomicAdd(&s_nh, (u32)__popc(bal));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (found) hlist[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
-            });
-        }
-        __syncthreads();
-        // phase 2: stream the H-edges
-        const u32 nh = s_nh;
-        for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
-            const uint2 he = hlist[h];
-            const u32 i = he.x & 0xffffu, j = he.x >> 16;
-            const u32* ri = rows + (u64)i * W;
-            const u32* rj = rows + (u64)j * W;
-            u32 c = 0;
-            for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
-            atomicAdd(&t[he.y], 1u);
-            if (c) {
-                atomicAdd(&tri[i], c);
-                atomicAdd(&tri[j], c);
-                atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
             }
         }
         __syncthreads();
-        // phase 3: edges (a, x_i)
-        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-            u32 deg = 0;
-            const u32* ri = rows + (u64)i * W;
-            for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
-            const u32 e = g.eid[ub + i];
-            if (deg) atomicAdd(&t[e], deg);
-            if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
+        if (MODE == kHPassCount) {
+            // phase 2: stream the H-edges
+            const u32 nh = s_nh;
+            for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
+                const uint2 he = hlist[h];
+                const u32 i = he.x & 0xffffu, j = he.x >> 16;
+                const u32* ri = rows + (u64)i * W;
+                const u32* rj = rows + (u64)j * W;
+                u32 c = 0;
+                for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
+                atomicAdd(&t[he.y], 1u);
+                if (c) {
+                    atomicAdd(&tri[i], c);
+                    atomicAdd(&tri[j], c);
+                    atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
+                }
+            }
+            __syncthreads();
+            // phase 3: edges (a, x_i)
+            for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+                u32 deg = 0;
+                const u32* ri = rows + (u64)i * W;
+                for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
+                const u32 e = g.eid[ub + i];
+                if (deg) atomicAdd(&t[e], deg);
+                if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
+            }
+        } else {
+            for (u32 i = threadIdx.x; i < k; i += blockDim.x)
+                if (acc[i]) atomic_add_i64(&part[2 * (u64)g.eid[ub + i] + 1], -(i64)acc[i]);
         }
     }
 }
@@ -973,7 +937,7 @@ __global__ void k_seq(u32* __restrict__ ids, u64 n) {
 }
 
 // H-pass work list key: big-k (k > 32) items first, each class ordered by its
-// probe count Q(a) = sum_i min(|U(x_i)|, k-1-i) (the phase-1 work).
+// streaming cost s1(a) = sum_{i<k-1} |U(x_i)| (adjacency entries read).
 constexpr u64 kHBigFlag = 1ull << 40;
 __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     u32 mx = 0;
@@ -987,8 +951,9 @@ __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     }
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
-__global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* __restrict__ cnt) {
-    unsigned long long lb = 0, ls = 0;
+__global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* __restrict__ cnt,
+                        unsigned long long* __restrict__ s1_total) {
+    unsigned long long lb = 0, ls = 0, st = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         const u64 ub = g.off[a] + g.lcnt[a];
         const u64 k = g.off[a + 1] - ub;
@@ -997,10 +962,9 @@ __global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* 
             u64 q = 0;
             for (u64 i = 0; i + 1 < k; ++i) {
                 const u32 x = g.adj[ub + i];
-                const u64 lu = g.off[x + 1] - (g.off[x] + g.lcnt[x]);
-                const u64 rem = k - 1 - i;
-                q += lu < rem ? lu : rem;
+                q += g.off[x + 1] - (g.off[x] + g.lcnt[x]);
             }
+            st += q;
             key = (k > (u64)kHWarpMax ? kHBigFlag : 0) | (q + 1);
             if (k > (u64)kHWarpMax)
                 ++lb;
@@ -1011,6 +975,7 @@ __global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* 
     }
     if (lb) atomicAdd(&cnt[0], lb);
     if (ls) atomicAdd(&cnt[1], ls);
+    if (st) atomicAdd(s1_total, st);
 }
 
 // cycle work list key = wedges of top a; classes big (> kMidWedges, dense
@@ -1112,7 +1077,6 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     std::memset(cs.work, 0, sizeof(cs.work));
 
     cs.t.alloc((m + 1) * sizeof(u32));
-    cs.pre1.alloc((m + 1) * sizeof(u64));
     cs.wpre.alloc((m + 1) * sizeof(u64));
     cs.acc.alloc(64 * sizeof(u64));
     cs.keys.alloc((std::max(m, n) + 1) * 2 * sizeof(u64)); // key in/out
@@ -1130,67 +1094,66 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     if (m == 0) {
         for (int i = 1; i < 3; ++i) GL_CUDA(cudaEventRecord(tm.ev[i], s));
     } else {
-        u64* probes = cs.keys.as<u64>(); // scratch reuse before the sorts
-        u64* wedges = probes + (m + 1);
-        k_prepass<<<grid1d(m, 256, sms), 256, 0, s>>>(g, probes, wedges, counters + 17);
+        u64* wedges = cs.keys.as<u64>(); // scratch reuse before the sorts
+        k_prepass<<<grid1d(m, 256, sms), 256, 0, s>>>(g, wedges);
         GL_LAUNCH_CHECK();
-        GL_CUDA(cudaMemsetAsync(probes + m, 0, sizeof(u64), s));
         GL_CUDA(cudaMemsetAsync(wedges + m, 0, sizeof(u64), s));
-        dev_exclusive_scan<u64>(cs.tmp, probes, cs.pre1.as<u64>(), m + 1, s);
         dev_exclusive_scan<u64>(cs.tmp, wedges, cs.wpre.as<u64>(), m + 1, s);
-        cs.launches += 5;
-        cs.probes = read_dev(cs.pre1.as<u64>() + m, s);
-        cs.lsum = read_dev<unsigned long long>(counters + 17, s);
-        cs.work[0] = 4 * cs.lsum / (u64)world; // H-pass builds every H_a row by intersection
+        cs.launches += 2;
 
-        // H-pass: vertices by |U(a)| descending; k > 32 block kernel, else warp kernel
+        // H-pass: vertices by streaming cost descending; k > 32 block kernel, else warp kernel.
+        // The rank's lists stay in items3b / items3s for the triangle-sum pass (count_mid).
         {
             u64* kin = cs.keys.as<u64>();
             u64* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
-            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12);
+            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17);
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
             cs.launches += 2 + 10;
             const u64 nbig = read_dev<unsigned long long>(counters + 12, s);
             const u64 nsmall = read_dev<unsigned long long>(counters + 13, s);
+            cs.s1 = read_dev<unsigned long long>(counters + 17, s);
+            cs.work[0] = 4 * cs.s1 / (u64)world; // adjacency bytes streamed by the intersections
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
-            u32* lbig = iin;
-            u32* lsmall = iin + mybig;
+            cs.n_items3b = mybig;
+            cs.n_items3s = mysmall;
+            cs.items3b.alloc((mybig + 1) * sizeof(u32));
+            cs.items3s.alloc((mysmall + 1) * sizeof(u32));
             if (mybig) {
-                const u64 qmax = (read_dev(kout, s) & (kHBigFlag - 1)) - 1;
-                k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
+                const u64 s1max = (read_dev(kout, s) & (kHBigFlag - 1)) - 1;
+                k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, cs.items3b.as<u32>());
                 GL_LAUNCH_CHECK();
                 const unsigned blocks = (unsigned)sms * 2;
                 k_umax<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 14));
                 GL_LAUNCH_CHECK();
                 const u32 kmax = (u32)read_dev<unsigned long long>(counters + 14, s);
                 if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
-                u64 gstride = 0;
+                cs.h_gstride = 0;
                 if (kmax > (u32)kHSmemMax) {
-                    gstride = 3ull * kmax + 1 + (u64)kmax * ((kmax + 31) / 32);
-                    cs.scratch.alloc((u64)blocks * gstride * sizeof(u32));
+                    cs.h_gstride = (hpass_ws_words(kmax) + 1) & ~1ull;
+                    cs.scratch.alloc((u64)blocks * cs.h_gstride * sizeof(u32));
                 }
-                if (qmax >= (1ull << 32)) throw overflow_error("H-pass probe count exceeds 32 bits");
-                cs.hlist.alloc((u64)blocks * (qmax + 1) * sizeof(uint2));
-                const u32 ks = (u32)kHSmemMax;
-                const size_t smem = (size_t)(3ull * ks + 1 + (u64)ks * ((ks + 31) / 32)) * sizeof(u32);
-                GL_CUDA(cudaFuncSetAttribute(k_hclique_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                const u64 hcap = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
+                cs.hlist.alloc((u64)blocks * hcap * sizeof(uint2));
+                const size_t smem = (size_t)hpass_ws_words(kHSmemMax) * sizeof(u32);
+                GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
-                k_hclique_block<<<blocks, kHBlockThreads, smem, s>>>(
-                    g, lbig, mybig, counters + 0, cs.t.as<u32>(), d_partials,
-                    gstride ? cs.scratch.as<u32>() : nullptr, gstride, cs.hlist.as<uint2>(), qmax + 1);
+                k_hpass_block<kHPassCount><<<blocks, kHBlockThreads, smem, s>>>(
+                    g, cs.items3b.as<u32>(), mybig, counters + 0, cs.t.as<u32>(), d_partials,
+                    cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, cs.hlist.as<uint2>(), hcap);
                 GL_LAUNCH_CHECK();
-                cs.launches += 2;
+                cs.launches += 3;
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig, nsmall, rank, world, lsmall);
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig, nsmall, rank, world,
+                                                                      cs.items3s.as<u32>());
                 GL_LAUNCH_CHECK();
-                k_hclique_warp<<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
-                    g, lsmall, mysmall, counters + 3, cs.t.as<u32>(), d_partials);
+                k_hpass_warp<kHPassCount><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
+                    g, cs.items3s.as<u32>(), mysmall, counters + 3, cs.t.as<u32>(), d_partials);
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
             }
@@ -1281,15 +1244,26 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     const int sms = num_sms(gr.device);
     Timer tm(2);
     GL_CUDA(cudaEventRecord(tm.ev[0], s));
-    const u64 P = cs.probes;
-    const u64 b = P * (u64)cs.rank / cs.world, en = P * (u64)(cs.rank + 1) / cs.world;
-    if (g.m && en > b) {
-        unsigned gs = (unsigned)std::min<u64>((en - b + kTriTile - 1) / kTriTile, (u64)sms * 8);
-        k_trisum<<<gs, kTriThreads, 0, s>>>(g, cs.pre1.as<u64>(), b, en, cs.t.as<u32>(), d_partials);
+    // triangle sums over the same vertex shares as this rank's H-pass
+    unsigned long long* counters = cs.acc.as<unsigned long long>() + 40;
+    if (g.m && cs.n_items3b) {
+        const unsigned blocks = (unsigned)sms * 2;
+        const size_t smem = (size_t)hpass_ws_words(kHSmemMax) * sizeof(u32);
+        GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassSums>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        k_hpass_block<kHPassSums><<<blocks, kHBlockThreads, smem, s>>>(
+            g, cs.items3b.as<u32>(), cs.n_items3b, counters + 5, cs.t.as<u32>(), d_partials,
+            cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, nullptr, 0);
         GL_LAUNCH_CHECK();
         cs.launches += 1;
-        cs.work[1] = (u64)((double)(4 * cs.lsum) * (double)(en - b) / (double)P);
     }
+    if (g.m && cs.n_items3s) {
+        k_hpass_warp<kHPassSums><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
+            g, cs.items3s.as<u32>(), cs.n_items3s, counters + 6, cs.t.as<u32>(), d_partials);
+        GL_LAUNCH_CHECK();
+        cs.launches += 1;
+    }
+    cs.work[1] = cs.work[0];
     GL_CUDA(cudaEventRecord(tm.ev[1], s));
     GL_CUDA(cudaEventSynchronize(tm.ev[1]));
     GL_CUDA(cudaEventElapsedTime(&cs.ms[1], tm.ev[0], tm.ev[1]));

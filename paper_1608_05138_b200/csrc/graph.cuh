@@ -64,7 +64,6 @@ struct CountState {
     DevBuf part;     // i64[2m]  partials for the single-process path
     DevBuf slots;    // i64[2m]  C4 credits per adjacency slot (folded into y)
     DevBuf hlist;    // per-block H-edge lists of the clique pass
-    DevBuf pre1;     // u64[m+1] probe prefix for the triangle kernels
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3b; // work lists
     DevBuf keys, tmp, scratch, cursor, acc; // sort keys, cub temp, kernel scratch
@@ -74,7 +73,7 @@ struct CountState {
     bool began = false;
     bool mid_done = false;
     int rank = 0, world = 1;
-    u64 probes = 0, lsum = 0;
+    u64 s1 = 0, h_gstride = 0; // H-pass streamed entries, global workspace stride
     float ms[5] = {0, 0, 0, 0, 0};
     u32 launches = 0;
     u64 work[4] = {0, 0, 0, 0};

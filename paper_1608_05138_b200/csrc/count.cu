@@ -100,7 +100,14 @@ constexpr int kHPassCount = 0, kHPassSums = 1;
 constexpr int kHWarpMax = 32;       // 2 <= k <= 32: one warp, one u32 row per lane
 constexpr int kHWarpsPerBlock = 8;
 constexpr int kHBlockThreads = 512; // k > 32: one block per vertex
-constexpr int kHSmemMax = 768;      // k <= 768: workspace in shared memory
+constexpr int kHSmemMax = 512;      // k <= 512: workspace in shared memory
+constexpr int kHUnroll = 8;         // streamed rounds in flight per warp
+
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
 
 __device__ __forceinline__ u64 u_begin(const DevGraph& g, u32 x) { return g.off[x] + g.lcnt[x]; }
 
@@ -255,14 +262,16 @@ __device__ u32 block_exclusive_scan(u32* a, u32 n) {
 // (kHPassCount) streams the H-edge list: popcount of the two rows, one t and
 // one x7 credit per H-edge; phase 3 credits the edges (a, x_i).
 template <int MODE>
-__global__ void __launch_bounds__(kHBlockThreads)
+__global__ void __launch_bounds__(kHBlockThreads, 2)
 k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
               uint2* __restrict__ hlist_all, u64 hcap) {
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
     __shared__ u32 s_nh, s_mi;
+    __shared__ uint2 s_cbuf[kHBlockThreads / 32][32 * kHUnroll];
     const u32 lane = lane_id();
+    uint2* cbuf = s_cbuf[threadIdx.x >> 5];
     uint2* hlist = MODE == kHPassCount ? hlist_all + (u64)blockIdx.x * hcap : nullptr;
     for (;;) {
         __syncthreads();
@@ -321,25 +330,52 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if (i + 1 >= k) break;
             const u32 x = xs[i];
             const u64 xb = u_begin(g, x), xe = g.off[x + 1];
-            for (u64 p0 = xb; p0 < xe; p0 += 128) {
-                u32 yv[4];
+            u64 acc_i = 0; // kHPassSums: credit of (a, x_i), summed over the member
+            const u64 ti = MODE == kHPassSums ? (u64)ta[i] : 0;
+            for (u64 p0 = xb; p0 < xe; p0 += 32u * kHUnroll) {
+                // kHUnroll coalesced rounds in flight; Bloom-filter them, then
+                // compact the candidates into the warp's buffer so that the
+                // exact lookups and the hit work run with full lanes
+                u32 yv[kHUnroll];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kHUnroll; ++u) {
                     const u64 p = p0 + 32u * u + lane;
                     yv[u] = p < xe ? __ldg(g.adj + p) : kEmpty;
                 }
+                u32 cand = 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const u64 p = p0 + 32u * u + lane;
-                    const u32 y = yv[u];
+                for (int u = 0; u < kHUnroll; ++u) {
+                    const u32 bb = bloom_bit(yv[u]);
+                    if (yv[u] <= xmax && ((bloom[bb >> 5] >> (bb & 31)) & 1u)) cand |= 1u << u; // kEmpty > xmax
+                }
+                const u32 c = __popc(cand);
+                u32 pos = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const u32 o = __shfl_up_sync(0xffffffffu, pos, d);
+                    if (lane >= (u32)d) pos += o;
+                }
+                const u32 tot = __shfl_sync(0xffffffffu, pos, 31);
+                if (tot == 0) continue;
+                pos -= c;
+#pragma unroll
+                for (int u = 0; u < kHUnroll; ++u) {
+                    if ((cand >> u) & 1u) {
+                        cbuf[pos] = make_uint2(yv[u], 32u * u + lane);
+                        ++pos;
+                    }
+                }
+                __syncwarp();
+                for (u32 q0 = 0; q0 < tot; q0 += 32) {
+                    const u32 q = q0 + lane;
                     bool hit = false;
-                    u32 j = 0;
-                    const u32 bb = bloom_bit(y);
-                    if (y <= xmax && ((bloom[bb >> 5] >> (bb & 31)) & 1u)) { // kEmpty > xmax
-                        u32 h = (y * 0x9E3779B1u) >> (32 - hl);
+                    u32 j = 0, e = 0;
+                    if (q < tot) {
+                        const uint2 cy = cbuf[q];
+                        u32 h = (cy.x * 0x9E3779B1u) >> (32 - hl);
                         for (;;) {
                             const u32 kk = hkey[h];
-                            if (kk == y) {
+                            if (kk == cy.x) {
                                 hit = true;
                                 j = hval[h];
                                 break;
@@ -347,9 +383,8 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                             if (kk == kEmpty) break;
                             h = (h + 1) & (H - 1);
                         }
+                        if (hit) e = g.eid[p0 + cy.y];
                     }
-                    u32 e = 0;
-                    if (hit) e = g.eid[p];
                     if (MODE == kHPassCount) {
                         if (hit) {
                             atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
@@ -364,11 +399,17 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                         }
                     } else if (hit) {
                         const u64 txy = t[e];
-                        atomic_add_i64(&part[2 * (u64)e + 1], -(i64)((u64)ta[i] + ta[j]));
-                        atomicAdd(&acc[i], (unsigned long long)(ta[j] + txy));
-                        atomicAdd(&acc[j], (unsigned long long)(ta[i] + txy));
+                        const u64 tj = ta[j];
+                        atomic_add_i64(&part[2 * (u64)e + 1], -(i64)(ti + tj));
+                        acc_i += tj + txy;
+                        atomicAdd(&acc[j], (unsigned long long)(ti + txy));
                     }
                 }
+                __syncwarp();
+            }
+            if (MODE == kHPassSums) {
+                acc_i = warp_sum_u64(acc_i);
+                if (lane == 0 && acc_i) atomicAdd(&acc[i], (unsigned long long)acc_i);
             }
         }
         __syncthreads();
@@ -406,11 +447,6 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     }
 }
 
-__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    return v;
-}
 
 // ------------------------------------------------------------------ cycles
 

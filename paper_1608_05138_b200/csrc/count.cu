@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 #include <vector>
 
@@ -100,7 +101,7 @@ constexpr int kHPassCount = 0, kHPassSums = 1;
 constexpr int kHWarpMax = 32;       // 2 <= k <= 32: one warp, one u32 row per lane
 constexpr int kHWarpsPerBlock = 8;
 constexpr int kHBlockThreads = 512; // k > 32: one block per vertex
-constexpr int kHSmemMax = 512;      // k <= 512: workspace in shared memory
+constexpr int kHSmemMax = 768;      // k <= 768: workspace in shared memory
 constexpr int kHUnroll = 8;         // streamed rounds in flight per warp
 
 __device__ __forceinline__ u64 warp_sum_u64(u64 v) {
@@ -114,18 +115,18 @@ __device__ __forceinline__ u64 u_begin(const DevGraph& g, u32 x) { return g.off[
 constexpr u32 kBloomLog = 16, kBloomWords = (1u << kBloomLog) / 32; // 8 KB member filter
 __device__ __forceinline__ u32 bloom_bit(u32 y) { return (y * 0x2545F491u) >> (32 - kBloomLog); }
 
-__device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 4k, >= 128
-    u32 l = 32 - __clz(4 * k - 1);
-    return l < 7 ? 7 : l;
+__device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 2k, >= 64 (Bloom filters the misses)
+    u32 l = 32 - __clz(2 * k - 1);
+    return l < 6 ? 6 : l;
 }
-__host__ __device__ inline u64 hpass_ws_words(u32 k) {
-    u32 l = 7;
-    while ((1u << l) < 4 * k) ++l;
+__host__ __device__ inline u64 hpass_ws_words(u32 k, int mode) {
+    u32 l = 6;
+    while ((1u << l) < 2 * k) ++l;
     const u64 H = 1ull << l;
     const u64 W = (k + 31) / 32;
-    const u64 count_ws = 2ull * k + (u64)k * W;  // xs, tri, rows
-    const u64 sums_ws = 4ull * k + 2;            // xs, ta, acc (u64, aligned)
-    return (count_ws > sums_ws ? count_ws : sums_ws) + 2 + H + H / 2 + kBloomWords;
+    const u64 body = mode == 0 ? 2ull * k + (u64)k * W  // xs, tri, rows
+                               : 4ull * k + 2;          // xs, ta, acc (u64, aligned)
+    return body + 2 + H + H / 2 + kBloomWords;
 }
 
 __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
@@ -269,9 +270,13 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
     __shared__ u32 s_nh, s_mi;
-    __shared__ uint2 s_cbuf[kHBlockThreads / 32][32 * kHUnroll];
+    // per-warp candidate buffer: (y, offset) for the sums pass; the counting
+    // pass keeps offsets only (its bitmap rows need the shared memory) and
+    // re-reads y from L1
+    using Cand = typename std::conditional<MODE == kHPassSums, uint2, unsigned short>::type;
+    __shared__ Cand s_cbuf[kHBlockThreads / 32][32 * kHUnroll];
     const u32 lane = lane_id();
-    uint2* cbuf = s_cbuf[threadIdx.x >> 5];
+    Cand* cbuf = s_cbuf[threadIdx.x >> 5];
     uint2* hlist = MODE == kHPassCount ? hlist_all + (u64)blockIdx.x * hcap : nullptr;
     for (;;) {
         __syncthreads();
@@ -361,7 +366,10 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
 #pragma unroll
                 for (int u = 0; u < kHUnroll; ++u) {
                     if ((cand >> u) & 1u) {
-                        cbuf[pos] = make_uint2(yv[u], 32u * u + lane);
+                        if constexpr (MODE == kHPassSums)
+                            cbuf[pos] = make_uint2(yv[u], 32u * u + lane);
+                        else
+                            cbuf[pos] = (unsigned short)(32u * u + lane);
                         ++pos;
                     }
                 }
@@ -371,11 +379,18 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                     bool hit = false;
                     u32 j = 0, e = 0;
                     if (q < tot) {
-                        const uint2 cy = cbuf[q];
-                        u32 h = (cy.x * 0x9E3779B1u) >> (32 - hl);
+                        u32 off, y;
+                        if constexpr (MODE == kHPassSums) {
+                            off = cbuf[q].y;
+                            y = cbuf[q].x;
+                        } else {
+                            off = cbuf[q];
+                            y = __ldg(g.adj + p0 + off); // L1-hot: this warp just read it
+                        }
+                        u32 h = (y * 0x9E3779B1u) >> (32 - hl);
                         for (;;) {
                             const u32 kk = hkey[h];
-                            if (kk == cy.x) {
+                            if (kk == y) {
                                 hit = true;
                                 j = hval[h];
                                 break;
@@ -383,7 +398,7 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                             if (kk == kEmpty) break;
                             h = (h + 1) & (H - 1);
                         }
-                        if (hit) e = g.eid[p0 + cy.y];
+                        if (hit) e = g.eid[p0 + off];
                     }
                     if (MODE == kHPassCount) {
                         if (hit) {
@@ -1170,12 +1185,12 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
                 cs.h_gstride = 0;
                 if (kmax > (u32)kHSmemMax) {
-                    cs.h_gstride = (hpass_ws_words(kmax) + 1) & ~1ull;
+                    cs.h_gstride = (hpass_ws_words(kmax, kHPassCount) + 1) & ~1ull;
                     cs.scratch.alloc((u64)blocks * cs.h_gstride * sizeof(u32));
                 }
                 const u64 hcap = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
                 cs.hlist.alloc((u64)blocks * hcap * sizeof(uint2));
-                const size_t smem = (size_t)hpass_ws_words(kHSmemMax) * sizeof(u32);
+                const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassCount) * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
                 k_hpass_block<kHPassCount><<<blocks, kHBlockThreads, smem, s>>>(
@@ -1284,7 +1299,7 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40;
     if (g.m && cs.n_items3b) {
         const unsigned blocks = (unsigned)sms * 2;
-        const size_t smem = (size_t)hpass_ws_words(kHSmemMax) * sizeof(u32);
+        const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassSums) * sizeof(u32);
         GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassSums>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         k_hpass_block<kHPassSums><<<blocks, kHBlockThreads, smem, s>>>(

@@ -262,6 +262,181 @@ __device__ u32 block_exclusive_scan(u32* a, u32 n) {
 // phase 1 streams the members' upper lists (warps grab members), phase 2
 // (kHPassCount) streams the H-edge list: popcount of the two rows, one t and
 // one x7 credit per H-edge; phase 3 credits the edges (a, x_i).
+// One vertex a of the block H-pass.  Inlined twice, with ws = the dynamic
+// shared memory (k <= kHSmemMax: every workspace access compiles to LDS/STS/
+// ATOMS) or the block's global scratch (larger k).
+template <int MODE, typename Cand>
+__device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
+                                             Cand* cbuf, uint2* hlist, u32& s_nh, u32& s_mi, u32 a, u64 ub, u32 k,
+                                             u32 W, u32 hl, u32 H) {
+    const u32 lane = lane_id();
+    u32* xs = ws;
+    u32* tri = xs + k;                      // kHPassCount
+    u32* rows = tri + k;                    // kHPassCount
+    u32* ta = xs + k;                       // kHPassSums
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
+    const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * W : ((2ull * k + 1) & ~1ull) + 2ull * k;
+    u32* bloom = ws + body;
+    u32* hkey = bloom + kBloomWords;
+    unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
+    for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+        xs[i] = g.adj[ub + i];
+        if (MODE == kHPassCount) {
+            tri[i] = 0;
+        } else {
+            ta[i] = t[g.eid[ub + i]];
+            acc[i] = 0;
+        }
+    }
+    if (MODE == kHPassCount)
+        for (u64 w = threadIdx.x; w < (u64)k * W; w += blockDim.x) rows[w] = 0;
+    for (u32 h = threadIdx.x; h < H; h += blockDim.x) hkey[h] = kEmpty;
+    for (u32 w = threadIdx.x; w < kBloomWords; w += blockDim.x) bloom[w] = 0;
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+        const u32 x = xs[i];
+        u32 h = (x * 0x9E3779B1u) >> (32 - hl);
+        while (atomicCAS(&hkey[h], kEmpty, x) != kEmpty) h = (h + 1) & (H - 1);
+        hval[h] = (unsigned short)i;
+        const u32 bb = bloom_bit(x);
+        atomicOr(&bloom[bb >> 5], 1u << (bb & 31));
+    }
+    __syncthreads();
+    const u32 xmax = xs[k - 1];
+    // phase 1: warps grab members i < k-1 and stream U(x_i)
+    for (;;) {
+        u32 i = 0;
+        if (lane == 0) i = atomicAdd(&s_mi, 1u);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i + 1 >= k) break;
+        const u32 x = xs[i];
+        const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+        u64 acc_i = 0; // kHPassSums: credit of (a, x_i), summed over the member
+        const u64 ti = MODE == kHPassSums ? (u64)ta[i] : 0;
+        for (u64 p0 = xb; p0 < xe; p0 += 32u * kHUnroll) {
+            // kHUnroll coalesced rounds in flight; Bloom-filter them, then
+            // compact the candidates into the warp's buffer so that the
+            // exact lookups and the hit work run with full lanes
+            u32 yv[kHUnroll];
+#pragma unroll
+            for (int u = 0; u < kHUnroll; ++u) {
+                const u64 p = p0 + 32u * u + lane;
+                yv[u] = p < xe ? __ldg(g.adj + p) : kEmpty;
+            }
+            u32 cand = 0;
+#pragma unroll
+            for (int u = 0; u < kHUnroll; ++u) {
+                const u32 bb = bloom_bit(yv[u]);
+                if (yv[u] <= xmax && ((bloom[bb >> 5] >> (bb & 31)) & 1u)) cand |= 1u << u; // kEmpty > xmax
+            }
+            const u32 c = __popc(cand);
+            u32 pos = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const u32 o = __shfl_up_sync(0xffffffffu, pos, d);
+                if (lane >= (u32)d) pos += o;
+            }
+            const u32 tot = __shfl_sync(0xffffffffu, pos, 31);
+            if (tot == 0) continue;
+            pos -= c;
+#pragma unroll
+            for (int u = 0; u < kHUnroll; ++u) {
+                if ((cand >> u) & 1u) {
+                    if constexpr (MODE == kHPassSums)
+                        cbuf[pos] = make_uint2(yv[u], 32u * u + lane);
+                    else
+                        cbuf[pos] = (unsigned short)(32u * u + lane);
+                    ++pos;
+                }
+            }
+            __syncwarp();
+            for (u32 q0 = 0; q0 < tot; q0 += 32) {
+                const u32 q = q0 + lane;
+                bool hit = false;
+                u32 j = 0, e = 0;
+                if (q < tot) {
+                    u32 off, y;
+                    if constexpr (MODE == kHPassSums) {
+                        off = cbuf[q].y;
+                        y = cbuf[q].x;
+                    } else {
+                        off = cbuf[q];
+                        y = __ldg(g.adj + p0 + off); // L1-hot: this warp just read it
+                    }
+                    u32 h = (y * 0x9E3779B1u) >> (32 - hl);
+                    for (;;) {
+                        const u32 kk = hkey[h];
+                        if (kk == y) {
+                            hit = true;
+                            j = hval[h];
+                            break;
+                        }
+                        if (kk == kEmpty) break;
+                        h = (h + 1) & (H - 1);
+                    }
+                    if (hit) e = g.eid[p0 + off];
+                }
+                if (MODE == kHPassCount) {
+                    if (hit) {
+                        atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
+                        atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (bal) {
+                        u32 base = 0;
+                        if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (hit) hlist[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
+                    }
+                } else if (hit) {
+                    const u64 txy = t[e];
+                    const u64 tj = ta[j];
+                    atomic_add_i64(&part[2 * (u64)e + 1], -(i64)(ti + tj));
+                    acc_i += tj + txy;
+                    atomicAdd(&acc[j], (unsigned long long)(ti + txy));
+                }
+            }
+            __syncwarp();
+        }
+        if (MODE == kHPassSums) {
+            acc_i = warp_sum_u64(acc_i);
+            if (lane == 0 && acc_i) atomicAdd(&acc[i], (unsigned long long)acc_i);
+        }
+    }
+    __syncthreads();
+    if (MODE == kHPassCount) {
+        // phase 2: stream the H-edges
+        const u32 nh = s_nh;
+        for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
+            const uint2 he = hlist[h];
+            const u32 i = he.x & 0xffffu, j = he.x >> 16;
+            const u32* ri = rows + (u64)i * W;
+            const u32* rj = rows + (u64)j * W;
+            u32 c = 0;
+            for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
+            atomicAdd(&t[he.y], 1u);
+            if (c) {
+                atomicAdd(&tri[i], c);
+                atomicAdd(&tri[j], c);
+                atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
+            }
+        }
+        __syncthreads();
+        // phase 3: edges (a, x_i)
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+            u32 deg = 0;
+            const u32* ri = rows + (u64)i * W;
+            for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
+            const u32 e = g.eid[ub + i];
+            if (deg) atomicAdd(&t[e], deg);
+            if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
+        }
+    } else {
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x)
+            if (acc[i]) atomic_add_i64(&part[2 * (u64)g.eid[ub + i] + 1], -(i64)acc[i]);
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kHBlockThreads, 2)
 k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
@@ -293,172 +468,14 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 k = (u32)(g.off[a + 1] - ub);
         const u32 W = (k + 31) >> 5;
         const u32 hl = hp_log(k), H = 1u << hl;
-        u32* ws = k <= (u32)kHSmemMax ? smem : gscratch + (u64)blockIdx.x * gstride;
-        u32* xs = ws;
-        u32* tri = xs + k;                      // kHPassCount
-        u32* rows = tri + k;                    // kHPassCount
-        u32* ta = xs + k;                       // kHPassSums
-        unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
-        const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * W : ((2ull * k + 1) & ~1ull) + 2ull * k;
-        u32* bloom = ws + body;
-        u32* hkey = bloom + kBloomWords;
-        unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
-        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-            xs[i] = g.adj[ub + i];
-            if (MODE == kHPassCount) {
-                tri[i] = 0;
-            } else {
-                ta[i] = t[g.eid[ub + i]];
-                acc[i] = 0;
-            }
-        }
-        if (MODE == kHPassCount)
-            for (u64 w = threadIdx.x; w < (u64)k * W; w += blockDim.x) rows[w] = 0;
-        for (u32 h = threadIdx.x; h < H; h += blockDim.x) hkey[h] = kEmpty;
-        for (u32 w = threadIdx.x; w < kBloomWords; w += blockDim.x) bloom[w] = 0;
-        __syncthreads();
-        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-            const u32 x = xs[i];
-            u32 h = (x * 0x9E3779B1u) >> (32 - hl);
-            while (atomicCAS(&hkey[h], kEmpty, x) != kEmpty) h = (h + 1) & (H - 1);
-            hval[h] = (unsigned short)i;
-            const u32 bb = bloom_bit(x);
-            atomicOr(&bloom[bb >> 5], 1u << (bb & 31));
-        }
-        __syncthreads();
-        const u32 xmax = xs[k - 1];
-        // phase 1: warps grab members i < k-1 and stream U(x_i)
-        for (;;) {
-            u32 i = 0;
-            if (lane == 0) i = atomicAdd(&s_mi, 1u);
-            i = __shfl_sync(0xffffffffu, i, 0);
-            if (i + 1 >= k) break;
-            const u32 x = xs[i];
-            const u64 xb = u_begin(g, x), xe = g.off[x + 1];
-            u64 acc_i = 0; // kHPassSums: credit of (a, x_i), summed over the member
-            const u64 ti = MODE == kHPassSums ? (u64)ta[i] : 0;
-            for (u64 p0 = xb; p0 < xe; p0 += 32u * kHUnroll) {
-                // kHUnroll coalesced rounds in flight; Bloom-filter them, then
-                // compact the candidates into the warp's buffer so that the
-                // exact lookups and the hit work run with full lanes
-                u32 yv[kHUnroll];
-#pragma unroll
-                for (int u = 0; u < kHUnroll; ++u) {
-                    const u64 p = p0 + 32u * u + lane;
-                    yv[u] = p < xe ? __ldg(g.adj + p) : kEmpty;
-                }
-                u32 cand = 0;
-#pragma unroll
-                for (int u = 0; u < kHUnroll; ++u) {
-                    const u32 bb = bloom_bit(yv[u]);
-                    if (yv[u] <= xmax && ((bloom[bb >> 5] >> (bb & 31)) & 1u)) cand |= 1u << u; // kEmpty > xmax
-                }
-                const u32 c = __popc(cand);
-                u32 pos = c;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const u32 o = __shfl_up_sync(0xffffffffu, pos, d);
-                    if (lane >= (u32)d) pos += o;
-                }
-                const u32 tot = __shfl_sync(0xffffffffu, pos, 31);
-                if (tot == 0) continue;
-                pos -= c;
-#pragma unroll
-                for (int u = 0; u < kHUnroll; ++u) {
-                    if ((cand >> u) & 1u) {
-                        if constexpr (MODE == kHPassSums)
-                            cbuf[pos] = make_uint2(yv[u], 32u * u + lane);
-                        else
-                            cbuf[pos] = (unsigned short)(32u * u + lane);
-                        ++pos;
-                    }
-                }
-                __syncwarp();
-                for (u32 q0 = 0; q0 < tot; q0 += 32) {
-                    const u32 q = q0 + lane;
-                    bool hit = false;
-                    u32 j = 0, e = 0;
-                    if (q < tot) {
-                        u32 off, y;
-                        if constexpr (MODE == kHPassSums) {
-                            off = cbuf[q].y;
-                            y = cbuf[q].x;
-                        } else {
-                            off = cbuf[q];
-                            y = __ldg(g.adj + p0 + off); // L1-hot: this warp just read it
-                        }
-                        u32 h = (y * 0x9E3779B1u) >> (32 - hl);
-                        for (;;) {
-                            const u32 kk = hkey[h];
-                            if (kk == y) {
-                                hit = true;
-                                j = hval[h];
-                                break;
-                            }
-                            if (kk == kEmpty) break;
-                            h = (h + 1) & (H - 1);
-                        }
-                        if (hit) e = g.eid[p0 + off];
-                    }
-                    if (MODE == kHPassCount) {
-                        if (hit) {
-                            atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
-                            atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
-                        }
-                        const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                        if (bal) {
-                            u32 base = 0;
-                            if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
-                            base = __shfl_sync(0xffffffffu, base, 0);
-                            if (hit) hlist[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
-                        }
-                    } else if (hit) {
-                        const u64 txy = t[e];
-                        const u64 tj = ta[j];
-                        atomic_add_i64(&part[2 * (u64)e + 1], -(i64)(ti + tj));
-                        acc_i += tj + txy;
-                        atomicAdd(&acc[j], (unsigned long long)(ti + txy));
-                    }
-                }
-                __syncwarp();
-            }
-            if (MODE == kHPassSums) {
-                acc_i = warp_sum_u64(acc_i);
-                if (lane == 0 && acc_i) atomicAdd(&acc[i], (unsigned long long)acc_i);
-            }
-        }
-        __syncthreads();
-        if (MODE == kHPassCount) {
-            // phase 2: stream the H-edges
-            const u32 nh = s_nh;
-            for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
-                const uint2 he = hlist[h];
-                const u32 i = he.x & 0xffffu, j = he.x >> 16;
-                const u32* ri = rows + (u64)i * W;
-                const u32* rj = rows + (u64)j * W;
-                u32 c = 0;
-                for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
-                atomicAdd(&t[he.y], 1u);
-                if (c) {
-                    atomicAdd(&tri[i], c);
-                    atomicAdd(&tri[j], c);
-                    atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
-                }
-            }
-            __syncthreads();
-            // phase 3: edges (a, x_i)
-            for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-                u32 deg = 0;
-                const u32* ri = rows + (u64)i * W;
-                for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
-                const u32 e = g.eid[ub + i];
-                if (deg) atomicAdd(&t[e], deg);
-                if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
-            }
-        } else {
-            for (u32 i = threadIdx.x; i < k; i += blockDim.x)
-                if (acc[i]) atomic_add_i64(&part[2 * (u64)g.eid[ub + i] + 1], -(i64)acc[i]);
-        }
+        if (MODE == kHPassSums) // one generic-pointer copy measured faster for the lighter sums pass
+            hpass_vertex<MODE>(g, t, part, k <= (u32)kHSmemMax ? smem : gscratch + (u64)blockIdx.x * gstride, cbuf,
+                               hlist, s_nh, s_mi, a, ub, k, W, hl, H);
+        else if (k <= (u32)kHSmemMax)
+            hpass_vertex<MODE>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H);
+        else
+            hpass_vertex<MODE>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a, ub,
+                               k, W, hl, H);
     }
 }
 

@@ -1006,7 +1006,15 @@ __global__ void k_seq(u32* __restrict__ ids, u64 n) {
 
 // H-pass work list key: big-k (k > 32) items first, each class ordered by its
 // streaming cost s1(a) = sum_{i<k-1} |U(x_i)| (adjacency entries read).
-constexpr u64 kHBigFlag = 1ull << 40;
+// Work lists only need an approximate cost order: keys are a 4-bit-mantissa
+// log2 of the cost (10 bits) under a class bit, so the radix sort runs over
+// 17 key bits instead of 64.
+constexpr u32 kKeyBits = 17, kClassBit = 1u << 16;
+__device__ __forceinline__ u32 log_key(u64 c) { // monotone in c, 0 for c = 0
+    if (c < 16) return (u32)c;
+    const u32 msb = 63 - __clzll(c);
+    return (msb << 4) | (u32)((c >> (msb - 4)) & 15u);
+}
 __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     u32 mx = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
@@ -1019,13 +1027,14 @@ __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     }
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
-__global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* __restrict__ cnt,
-                        unsigned long long* __restrict__ s1_total) {
+__global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* __restrict__ cnt,
+                        unsigned long long* __restrict__ s1_total, unsigned long long* __restrict__ s1_max) {
+    unsigned long long mx = 0;
     unsigned long long lb = 0, ls = 0, st = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         const u64 ub = g.off[a] + g.lcnt[a];
         const u64 k = g.off[a + 1] - ub;
-        u64 key = 0;
+        u32 key = 0;
         if (k >= 2) {
             u64 q = 0;
             for (u64 i = 0; i + 1 < k; ++i) {
@@ -1033,34 +1042,42 @@ __global__ void k_hkeys(DevGraph g, u64* __restrict__ keys, unsigned long long* 
                 q += g.off[x + 1] - (g.off[x] + g.lcnt[x]);
             }
             st += q;
-            key = (k > (u64)kHWarpMax ? kHBigFlag : 0) | (q + 1);
-            if (k > (u64)kHWarpMax)
+            key = (k > (u64)kHWarpMax ? kClassBit : 0u) | (log_key(q) + 1);
+            if (k > (u64)kHWarpMax) {
                 ++lb;
-            else
+                mx = q > mx ? q : mx;
+            } else {
                 ++ls;
+            }
         }
         keys[a] = key;
     }
     if (lb) atomicAdd(&cnt[0], lb);
     if (ls) atomicAdd(&cnt[1], ls);
     if (st) atomicAdd(s1_total, st);
+    if (mx) atomicMax(s1_max, mx);
 }
 
 // cycle work list key = wedges of top a; classes big (> kMidWedges, dense
 // windows), mid (> kSmallWedges, block hash), small (warp hash)
-__global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u64* __restrict__ keys,
+__global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u32* __restrict__ keys,
                            unsigned long long* __restrict__ n_big, unsigned long long* __restrict__ n_mid,
                            unsigned long long* __restrict__ n_small) {
     unsigned long long lb = 0, lm = 0, ls = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         u64 w = wpre[g.loff[a + 1]] - wpre[g.loff[a]];
-        keys[a] = w;
-        if (w > kMidWedges)
+        u32 cls = 0; // exact class boundaries: class above the log cost
+        if (w > kMidWedges) {
             ++lb;
-        else if (w > kSmallWedges)
+            cls = 3;
+        } else if (w > kSmallWedges) {
             ++lm;
-        else if (w)
+            cls = 2;
+        } else if (w) {
             ++ls;
+            cls = 1;
+        }
+        keys[a] = (cls << 12) | log_key(w);
     }
     if (lb) atomicAdd(n_big, lb);
     if (lm) atomicAdd(n_mid, lm);
@@ -1097,14 +1114,14 @@ void dev_exclusive_scan(DevBuf& tmp, const T* in, T* out, u64 n, cudaStream_t s)
 }
 
 // sort (key desc, id) pairs; ids_out sorted by descending key (stable)
-void dev_sort_desc(DevBuf& tmp, u64* keys_in, u64* keys_out, u32* ids_in, u32* ids_out, u64 n,
+void dev_sort_desc(DevBuf& tmp, u32* keys_in, u32* keys_out, u32* ids_in, u32* ids_out, u64 n,
                    cudaStream_t s) {
     size_t bytes = 0;
     GL_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, keys_in, keys_out, ids_in, ids_out,
-                                                      (int64_t)n, 0, 64, s));
+                                                      (int64_t)n, 0, (int)kKeyBits, s));
     tmp.alloc(bytes);
     GL_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, keys_in, keys_out, ids_in, ids_out,
-                                                      (int64_t)n, 0, 64, s));
+                                                      (int64_t)n, 0, (int)kKeyBits, s));
 }
 
 template <typename T> T read_dev(const T* p, cudaStream_t s) {
@@ -1172,11 +1189,11 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
         // H-pass: vertices by streaming cost descending; k > 32 block kernel, else warp kernel.
         // The rank's lists stay in items3b / items3s for the triangle-sum pass (count_mid).
         {
-            u64* kin = cs.keys.as<u64>();
-            u64* kout = kin + (n + 1);
+            u32* kin = cs.keys.as<u32>();
+            u32* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
-            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17);
+            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17, counters + 18);
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
@@ -1192,7 +1209,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             cs.items3b.alloc((mybig + 1) * sizeof(u32));
             cs.items3s.alloc((mysmall + 1) * sizeof(u32));
             if (mybig) {
-                const u64 s1max = (read_dev(kout, s) & (kHBigFlag - 1)) - 1;
+                const u64 s1max = read_dev<unsigned long long>(counters + 18, s);
                 k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, cs.items3b.as<u32>());
                 GL_LAUNCH_CHECK();
                 const unsigned blocks = (unsigned)sms * 2;
@@ -1231,8 +1248,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
 
         // cycles: top vertices, split small (warp hash) / big (block windows)
         {
-            u64* kin = cs.keys.as<u64>();
-            u64* kout = kin + (n + 1);
+            u32* kin = cs.keys.as<u32>();
+            u32* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
             k_top_keys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,

@@ -42,6 +42,7 @@ constexpr int kCycleSmallWarps = 8;  // warps per small-top block
 constexpr int kHashSlots = 1024;     // per-warp hash slots (small tops)
 constexpr u64 kSmallWedges = 512;    // small-top threshold (<= half the slots)
 constexpr int kBigThreads = 1024;    // block per big top (dense windows), one block per SM
+constexpr int kBigBlocksPerSM = 1;
 constexpr int kMidThreads = 1024;    // block per mid top (hash), one block per SM
 constexpr int kWindow = 32768;       // dense W window words (u32, or 2 x u16) in shared memory
 constexpr int kMidLog = 15;
@@ -249,6 +250,31 @@ __device__ u32 block_exclusive_scan(u32* a, u32 n) {
         u32 total;
         BlockScan(tmp).ExclusiveSum(v, v, total);
         const u32 carry = s_carry;
+        if (i0 < n) a[i0] = v[0] + carry;
+        if (i0 + 1 < n) a[i0 + 1] = v[1] + carry;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    return s_carry;
+}
+
+// In-place exclusive scan of n u64 by the whole block; returns the total.
+template <int THREADS>
+__device__ u64 block_exclusive_scan64(u64* a, u32 n) {
+    using BlockScan = cub::BlockScan<u64, THREADS>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ u64 s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (u32 base = 0; base < n; base += 2 * THREADS) {
+        u64 v[2];
+        const u32 i0 = base + 2 * threadIdx.x;
+        v[0] = i0 < n ? a[i0] : 0;
+        v[1] = i0 + 1 < n ? a[i0 + 1] : 0;
+        u64 total;
+        BlockScan(tmp).ExclusiveSum(v, v, total);
+        const u64 carry = s_carry;
         if (i0 < n) a[i0] = v[0] + carry;
         if (i0 + 1 < n) a[i0 + 1] = v[1] + carry;
         __syncthreads();
@@ -592,7 +618,7 @@ __device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
     u32 *cur, *hpos, *rend, *pre, *rj, *rs;
-    u64* rb;
+    u64 *rb, *pre64;
 };
 // compacted runs of one window: wedge prefix pre[nnz+1], first adjacency slot
 // rs[q] (u32: 2m < 2^32 is checked on the host), lower-neighbour index rj[q];
@@ -609,9 +635,10 @@ __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     s.rj = base + 4 * (u64)cap + 1;
     s.rs = base + 5 * (u64)cap + 1;
     s.rb = reinterpret_cast<u64*>(base + ((6 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
+    s.pre64 = s.rb + cap;
     return s;
 }
-__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 8ull * cap + 8; }
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 10ull * cap + 8; }
 
 // W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
 // or an open-addressing hash over all c < a (mid tops, HASH).  Hash keys are
@@ -810,7 +837,7 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
 }
 
 template <bool HASH>
-__global__ void __launch_bounds__(tab_threads(HASH), 1)
+__global__ void __launch_bounds__(tab_threads(HASH), HASH ? 1 : kBigBlocksPerSM)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
     constexpr int THREADS = tab_threads(HASH);
@@ -833,7 +860,9 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
         const bool half = HASH || nb < 65536u;
-        const u32 span = half ? 2u * kWindow : (u32)kWindow;
+        u32 span = half ? 2u * kWindow : (u32)kWindow;
+        // keep nb * span < 2^31: window wedge counts and indices are u32
+        if ((u64)nb * span >= (1ull << 31)) span = (u32)((1ull << 31) / nb) & ~1u;
         if (threadIdx.x == 0) s_next = HASH ? 0u : kEmpty;
         __syncthreads();
         // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at 0
@@ -847,63 +876,81 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if (!HASH && re > 0) atomicMin(&s_next, g.adj[rb]);
         }
         __syncthreads();
-        u32 lo = s_next;
-        while (lo != kEmpty && lo < a) {
+        // windows [lo, lo+span) from the smallest c on, fixed stride: the run
+        // of b in a window is [cur_b, nxt_b) and the window's ends become the
+        // next window's cursors (pointer swap, no extra pass)
+        u32* cur = S.cur;
+        u32* nxt = S.hpos;
+        for (u32 lo = s_next; lo < a; lo = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a)) {
             const u32 hi = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a);
-            // runs [cur, hpos) of every b; flag non-empty ones
+            // run ends; runs are ordered thread-major (thread t owns b = t + i*THREADS,
+            // coalesced), so one block scan of per-thread (runs, wedges) places them
+            u32 my_runs = 0, my_wedges = 0;
             for (u32 j = threadIdx.x; j < nb; j += THREADS) {
-                const u32 c0 = S.cur[j];
+                const u32 c0 = cur[j];
                 const u64 rb = S.rb[j];
                 const u32 h = HASH ? S.rend[j] : (u32)(gallop_lower_bound(g.adj, rb + c0, rb + S.rend[j], hi) - rb);
-                S.hpos[j] = h;
-                S.pre[j] = h > c0 ? 1u : 0u;
-            }
-            __syncthreads();
-            const u32 nnz = block_exclusive_scan<THREADS>(S.pre, nb);
-            const RunMeta M = nnz <= meta_cap(HASH) ? Msm : Mgl;
-            // compact: run j -> position pre[j] (global flags; M.pre is
-            // rewritten only after the compaction barrier)
-            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
-                const u32 c0 = S.cur[j], h = S.hpos[j];
+                nxt[j] = h;
                 if (h > c0) {
-                    const u32 q = S.pre[j];
-                    M.rj[q] = j;
-                    M.rs[q] = (u32)(S.rb[j] + c0);
+                    ++my_runs;
+                    my_wedges += h - c0;
                 }
             }
-            __syncthreads();
-            // run lengths in compacted order, then their prefix
-            for (u32 q = threadIdx.x; q < nnz; q += THREADS) {
-                const u32 j = M.rj[q];
-                M.pre[q] = S.hpos[j] - S.cur[j];
+            u64 tot;
+            u64 mine = ((u64)my_runs << 32) | my_wedges;
+            {
+                using BlockScan = cub::BlockScan<u64, THREADS>;
+                __shared__ typename BlockScan::TempStorage tmp;
+                BlockScan(tmp).ExclusiveSum(mine, mine, tot);
             }
+            const u32 nnz = (u32)(tot >> 32), T = (u32)tot;
+            const RunMeta M = nnz <= meta_cap(HASH) ? Msm : Mgl;
+            if (my_runs) {
+                u32 q = (u32)(mine >> 32), w = (u32)mine;
+                for (u32 j = threadIdx.x; j < nb; j += THREADS) {
+                    const u32 c0 = cur[j], h = nxt[j];
+                    if (h > c0) {
+                        M.rj[q] = j;
+                        M.rs[q] = (u32)(S.rb[j] + c0);
+                        M.pre[q] = w;
+                        ++q;
+                        w += h - c0;
+                    }
+                }
+            }
+            if (threadIdx.x == 0) M.pre[nnz] = T;
             if (threadIdx.x < 3) s_work[threadIdx.x] = 0;
             __syncthreads();
-            const u32 T = block_exclusive_scan<THREADS>(M.pre, nnz);
-            if (threadIdx.x == 0) M.pre[nnz] = T;
-            __syncthreads();
-            const bool bulk_clear = HASH || T > kWords / 8;
-            grab_pass<HASH, 0>(g, M, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
-            __syncthreads();
-            grab_pass<HASH, 1>(g, M, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
-            __syncthreads();
-            if (bulk_clear) {
-                const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
-                for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
-            } else if (!HASH) {
-                grab_pass<HASH, 2>(g, M, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+            if (T) {
+                const bool bulk_clear = HASH || T > kWords / 8;
+                {
+                    if (nnz <= meta_cap(HASH)) // shared-memory metadata: LDS in the walk
+                        grab_pass<HASH, 0>(g, Msm, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
+                    else
+                        grab_pass<HASH, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
+                }
+                __syncthreads();
+                {
+                    if (nnz <= meta_cap(HASH))
+                        grab_pass<HASH, 1>(g, Msm, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
+                    else
+                        grab_pass<HASH, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
+                }
+                __syncthreads();
+                if (bulk_clear) {
+                    const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
+                    for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
+                } else if (!HASH) {
+                    if (nnz <= meta_cap(HASH))
+                        grab_pass<HASH, 2>(g, Msm, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+                    else
+                        grab_pass<HASH, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+                }
             }
-            if (HASH) break;
-            // advance cursors, next non-empty window start
-            if (threadIdx.x == 0) s_next = kEmpty;
+            u32* tmp = cur;
+            cur = nxt;
+            nxt = tmp;
             __syncthreads();
-            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
-                const u32 h = S.hpos[j];
-                S.cur[j] = h;
-                if (h < S.rend[j]) atomicMin(&s_next, g.adj[S.rb[j] + h]);
-            }
-            __syncthreads();
-            lo = s_next;
         }
     }
 }
@@ -1279,7 +1326,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     const size_t smem = (size_t)smem_words(false) * sizeof(u32);
                     GL_CUDA(cudaFuncSetAttribute(k_cycle_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
-                    k_cycle_block<false><<<(unsigned)sms, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1,
+                    k_cycle_block<false><<<(unsigned)sms * kBigBlocksPerSM, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1,
                                                                           cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;

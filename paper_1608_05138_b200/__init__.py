@@ -38,7 +38,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libgraphlet_b200.so")
+    # GRAPHLET_B200_LIB selects another in-tree build of the same library
+    # (e.g. libgraphlet_b200_prof.so, the phase-instrumented variant)
+    return os.path.join(_HERE, os.environ.get("GRAPHLET_B200_LIB", "libgraphlet_b200.so"))
 
 
 if not os.path.exists(lib_path()):

@@ -836,6 +836,10 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
     }
 }
 
+#ifdef GL_CYCLE_PROF
+__device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..26] mid hash
+#endif
+
 template <bool HASH>
 __global__ void __launch_bounds__(tab_threads(HASH), HASH ? 1 : kBigBlocksPerSM)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
@@ -849,12 +853,35 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     const RunMeta Msm{W + kWords, W + kWords + meta_cap(HASH) + 1, W + kWords + 2 * meta_cap(HASH) + 1};
     const RunMeta Mgl{S.pre, S.rs, S.rj};
     for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
+#ifdef GL_CYCLE_PROF
+    // make prof: per-phase clock64 totals (thread 0, between barriers): 0 setup,
+    // 6 gallop, 1 scan, 2 compaction, 3 pass 0, 4 pass 1, 7 clear, 5 grab;
+    // 8 windows, 9 wedges, 10 tops (scripts/cycle_phases.py)
+    unsigned long long pf[11] = {0};
+    unsigned long long pt = clock64();
+#define GL_PROF_MARK(k)                                   \
+    if (threadIdx.x == 0) {                               \
+        const unsigned long long now_ = clock64();        \
+        pf[k] += now_ - pt;                               \
+        pt = now_;                                        \
+    }
+#define GL_PROF_SYNC_MARK(k) \
+    __syncthreads();         \
+    GL_PROF_MARK(k)
+#define GL_PROF_ADD(k, v) \
+    if (threadIdx.x == 0) pf[k] += (v);
+#else
+#define GL_PROF_MARK(k)
+#define GL_PROF_SYNC_MARK(k)
+#define GL_PROF_ADD(k, v)
+#endif
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
         __syncthreads();
         const unsigned long long idx = s_idx;
         if (idx >= n_items) break;
+        GL_PROF_MARK(5);
         const u32 a = items[idx];
         const u64 E0 = g.loff[a];
         const u32 nb = (u32)(g.loff[a + 1] - E0);
@@ -876,6 +903,8 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if (!HASH && re > 0) atomicMin(&s_next, g.adj[rb]);
         }
         __syncthreads();
+        GL_PROF_MARK(0);
+        GL_PROF_ADD(10, 1);
         // windows [lo, lo+span) from the smallest c on, fixed stride: the run
         // of b in a window is [cur_b, nxt_b) and the window's ends become the
         // next window's cursors (pointer swap, no extra pass)
@@ -896,6 +925,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                     my_wedges += h - c0;
                 }
             }
+            GL_PROF_SYNC_MARK(6);
             u64 tot;
             u64 mine = ((u64)my_runs << 32) | my_wedges;
             {
@@ -904,6 +934,9 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 BlockScan(tmp).ExclusiveSum(mine, mine, tot);
             }
             const u32 nnz = (u32)(tot >> 32), T = (u32)tot;
+            GL_PROF_MARK(1);
+            GL_PROF_ADD(8, 1);
+            GL_PROF_ADD(9, T);
             const RunMeta M = nnz <= meta_cap(HASH) ? Msm : Mgl;
             if (my_runs) {
                 u32 q = (u32)(mine >> 32), w = (u32)mine;
@@ -921,6 +954,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if (threadIdx.x == 0) M.pre[nnz] = T;
             if (threadIdx.x < 3) s_work[threadIdx.x] = 0;
             __syncthreads();
+            GL_PROF_MARK(2);
             if (T) {
                 const bool bulk_clear = HASH || T > kWords / 8;
                 {
@@ -930,6 +964,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                         grab_pass<HASH, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
                 }
                 __syncthreads();
+                GL_PROF_MARK(3);
                 {
                     if (nnz <= meta_cap(HASH))
                         grab_pass<HASH, 1>(g, Msm, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
@@ -937,6 +972,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                         grab_pass<HASH, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
                 }
                 __syncthreads();
+                GL_PROF_MARK(4);
                 if (bulk_clear) {
                     const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
                     for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
@@ -947,12 +983,18 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                         grab_pass<HASH, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
                 }
             }
+            GL_PROF_SYNC_MARK(7);
             u32* tmp = cur;
             cur = nxt;
             nxt = tmp;
             __syncthreads();
+            GL_PROF_MARK(5);
         }
     }
+#ifdef GL_CYCLE_PROF
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 11; ++k) atomicAdd(&g_cycle_prof[k + (HASH ? 16 : 0)], pf[k]);
+#endif
 }
 
 // y(e) += the two adjacency-slot accumulators of edge e (v's row, u's row).
@@ -1487,3 +1529,14 @@ void micro_records(const Graph& gr, u64 first, u64 count, u64* host_out) {
 }
 
 } // namespace gl
+
+#ifdef GL_CYCLE_PROF
+extern "C" int gl_debug_cycle_profile(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, gl::g_cycle_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return -4;
+    if (reset) {
+        unsigned long long z[32] = {0};
+        if (cudaMemcpyToSymbol(gl::g_cycle_prof, z, sizeof(z)) != cudaSuccess) return -4;
+    }
+    return 0;
+}
+#endif

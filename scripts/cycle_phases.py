@@ -1,0 +1,34 @@
+"""Per-phase clock64 totals of the dense-window cycle kernel (instrumented build):
+make -C paper_1608_05138_b200/csrc prof && GRAPHLET_B200_LIB=libgraphlet_b200_prof.so python scripts/cycle_phases.py [scale]"""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("GRAPHLET_B200_LIB", "libgraphlet_b200_prof.so")
+import paper_1608_05138_b200 as gl  # noqa: E402
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+g = gl.Graph.build(gl.generate_rmat(scale, 16, seed=1))
+def run():
+    try:
+        g.count()
+    except gl.GraphletError as e:  # timing experiments may break the counts on purpose
+        print("count error (ignored for timing):", e)
+
+
+run()
+buf = (C.c_ulonglong * 32)()
+gl.LIB.gl_debug_cycle_profile(buf, 1)
+run()
+gl.LIB.gl_debug_cycle_profile(buf, 0)
+names = ["setup", "scan", "compaction", "pass0", "pass1", "grab", "gallop", "clear"]
+for base, kind in ((0, "dense windows"), (16, "mid hash")):
+    tot = max(1, sum(buf[base:base + 8]))
+    print(f"== {kind}: {tot / 1e9:.2f} Gcyc summed over blocks")
+    for i, nm in enumerate(names):
+        if i == 8:
+            break
+        print(f"  {nm:12s} {buf[base + i] / 1e6:10.1f} Mcyc  {100 * buf[base + i] / tot:5.1f}%")
+    w, T, tops = buf[base + 8], buf[base + 9], buf[base + 10]
+    print(f"  windows {w}  wedges {T}  tops {tops}  wedges/window {T / max(1, w):.0f}")

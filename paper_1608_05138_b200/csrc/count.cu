@@ -291,11 +291,62 @@ __device__ u64 block_exclusive_scan64(u64* a, u32 n) {
 // One vertex a of the block H-pass.  Inlined twice, with ws = the dynamic
 // shared memory (k <= kHSmemMax: every workspace access compiles to LDS/STS/
 // ATOMS) or the block's global scratch (larger k).
+// Persistent H-edge records of the block H-pass: the counting pass appends
+// every H-edge (i | j << 16, e_xy) of vertex a to one device-wide list and
+// records (base, count) per work item; the triangle-sum pass then streams the
+// records instead of re-deriving them (base = kNoList: list full, re-derive).
+struct TriList {
+    uint2* rec;
+    u64 cap;
+    unsigned long long* count;
+    u64* base;   // per work item
+    u32* n;      // per work item
+};
+constexpr u64 kNoList = ~0ull;
+
 template <int MODE, typename Cand>
 __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
                                              Cand* cbuf, uint2* hlist, u32& s_nh, u32& s_mi, u32 a, u64 ub, u32 k,
-                                             u32 W, u32 hl, u32 H) {
+                                             u32 W, u32 hl, u32 H, const TriList& TL, u64 idx, u64& s_base) {
     const u32 lane = lane_id();
+    if (MODE == kHPassSums && TL.rec && TL.base[idx] != kNoList) {
+        // stream this vertex's H-edge records: t of (x_i, x_j) gathered, the
+        // (a, x) credits summed per member in shared memory
+        u32* ta = ws;
+        unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((k + 1) & ~1u));
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+            ta[i] = t[g.eid[ub + i]];
+            acc[i] = 0;
+        }
+        __syncthreads();
+        const uint2* rec = TL.rec + TL.base[idx];
+        const u32 nrec = TL.n[idx];
+        constexpr int U = 4;
+        for (u32 r0 = threadIdx.x; r0 < nrec; r0 += U * blockDim.x) {
+            uint2 rv[U];
+            u32 tv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const u32 r = r0 + u * blockDim.x;
+                rv[u] = r < nrec ? rec[r] : make_uint2(0, kEmpty);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) tv[u] = rv[u].y != kEmpty ? t[rv[u].y] : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (rv[u].y == kEmpty) continue;
+                const u32 i = rv[u].x & 0xffffu, j = rv[u].x >> 16;
+                const u64 ti = ta[i], tj = ta[j], txy = tv[u];
+                atomic_add_i64(&part[2 * (u64)rv[u].y + 1], -(i64)(ti + tj));
+                atomicAdd(&acc[i], (unsigned long long)(tj + txy));
+                atomicAdd(&acc[j], (unsigned long long)(ti + txy));
+            }
+        }
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x)
+            if (acc[i]) atomic_add_i64(&part[2 * (u64)g.eid[ub + i] + 1], -(i64)acc[i]);
+        return;
+    }
     u32* xs = ws;
     u32* tri = xs + k;                      // kHPassCount
     u32* rows = tri + k;                    // kHPassCount
@@ -431,10 +482,22 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     }
     __syncthreads();
     if (MODE == kHPassCount) {
-        // phase 2: stream the H-edges
+        // phase 2: stream the H-edges (and keep them for the sums pass)
         const u32 nh = s_nh;
+        if (TL.rec) {
+            if (threadIdx.x == 0) {
+                u64 b = atomicAdd(TL.count, (unsigned long long)nh);
+                if (b + nh > TL.cap) b = kNoList;
+                TL.base[idx] = b;
+                TL.n[idx] = nh;
+                s_base = b;
+            }
+            __syncthreads();
+        }
+        const u64 tb = TL.rec ? s_base : kNoList;
         for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
             const uint2 he = hlist[h];
+            if (tb != kNoList) TL.rec[tb + h] = he;
             const u32 i = he.x & 0xffffu, j = he.x >> 16;
             const u32* ri = rows + (u64)i * W;
             const u32* rj = rows + (u64)j * W;
@@ -467,9 +530,10 @@ template <int MODE>
 __global__ void __launch_bounds__(kHBlockThreads, 2)
 k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
-              uint2* __restrict__ hlist_all, u64 hcap) {
+              uint2* __restrict__ hlist_all, u64 hcap, TriList TL) {
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
+    __shared__ u64 s_base;
     __shared__ u32 s_nh, s_mi;
     // per-warp candidate buffer: (y, offset) for the sums pass; the counting
     // pass keeps offsets only (its bitmap rows need the shared memory) and
@@ -496,12 +560,12 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 hl = hp_log(k), H = 1u << hl;
         if (MODE == kHPassSums) // one generic-pointer copy measured faster for the lighter sums pass
             hpass_vertex<MODE>(g, t, part, k <= (u32)kHSmemMax ? smem : gscratch + (u64)blockIdx.x * gstride, cbuf,
-                               hlist, s_nh, s_mi, a, ub, k, W, hl, H);
+                               hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
         else if (k <= (u32)kHSmemMax)
-            hpass_vertex<MODE>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H);
+            hpass_vertex<MODE>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
         else
             hpass_vertex<MODE>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a, ub,
-                               k, W, hl, H);
+                               k, W, hl, H, TL, idx, s_base);
     }
 }
 
@@ -1117,8 +1181,9 @@ __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
 __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* __restrict__ cnt,
-                        unsigned long long* __restrict__ s1_total, unsigned long long* __restrict__ s1_max) {
-    unsigned long long mx = 0;
+                        unsigned long long* __restrict__ s1_total, unsigned long long* __restrict__ s1_max,
+                        unsigned long long* __restrict__ hedge_bound) {
+    unsigned long long mx = 0, hb = 0;
     unsigned long long lb = 0, ls = 0, st = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         const u64 ub = g.off[a] + g.lcnt[a];
@@ -1135,6 +1200,8 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
             if (k > (u64)kHWarpMax) {
                 ++lb;
                 mx = q > mx ? q : mx;
+                const u64 pairs = k * (k - 1) / 2;
+                hb += pairs < q ? pairs : q;
             } else {
                 ++ls;
             }
@@ -1145,6 +1212,7 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
     if (ls) atomicAdd(&cnt[1], ls);
     if (st) atomicAdd(s1_total, st);
     if (mx) atomicMax(s1_max, mx);
+    if (hb) atomicAdd(hedge_bound, hb);
 }
 
 // cycle work list key = wedges of top a; classes big (> kMidWedges, dense
@@ -1282,7 +1350,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
-            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17, counters + 18);
+            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17, counters + 18,
+                                                        counters + 19);
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
@@ -1313,12 +1382,24 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 }
                 const u64 hcap = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
                 cs.hlist.alloc((u64)blocks * hcap * sizeof(uint2));
+                // persistent H-edge records for the sums pass, up to ~40% of free memory
+                {
+                    const u64 bound = read_dev<unsigned long long>(counters + 19, s);
+                    size_t fr = 0, tot = 0;
+                    GL_CUDA(cudaMemGetInfo(&fr, &tot));
+                    const u64 cap = std::min<u64>(bound, (u64)(0.4 * (double)fr) / sizeof(uint2));
+                    cs.tl_cap = cap;
+                    cs.tlist.alloc((cap + 1) * sizeof(uint2));
+                    cs.tl_base.alloc((mybig + 1) * sizeof(u64));
+                    cs.tl_n.alloc((mybig + 1) * sizeof(u32));
+                }
                 const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassCount) * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
+                const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
                 k_hpass_block<kHPassCount><<<blocks, kHBlockThreads, smem, s>>>(
                     g, cs.items3b.as<u32>(), mybig, counters + 0, cs.t.as<u32>(), d_partials,
-                    cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, cs.hlist.as<uint2>(), hcap);
+                    cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, cs.hlist.as<uint2>(), hcap, TL);
                 GL_LAUNCH_CHECK();
                 cs.launches += 3;
             }
@@ -1425,9 +1506,10 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
         const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassSums) * sizeof(u32);
         GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassSums>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
+        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
         k_hpass_block<kHPassSums><<<blocks, kHBlockThreads, smem, s>>>(
             g, cs.items3b.as<u32>(), cs.n_items3b, counters + 5, cs.t.as<u32>(), d_partials,
-            cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, nullptr, 0);
+            cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, nullptr, 0, TL);
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     }

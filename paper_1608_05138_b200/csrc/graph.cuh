@@ -64,6 +64,8 @@ struct CountState {
     DevBuf part;     // i64[2m]  partials for the single-process path
     DevBuf slots;    // i64[2m]  C4 credits per adjacency slot (folded into y)
     DevBuf hlist;    // per-block H-edge lists of the clique pass
+    DevBuf tlist, tl_base, tl_n; // persistent H-edge records for the triangle-sum pass
+    u64 tl_cap = 0;
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3b; // work lists
     DevBuf keys, tmp, scratch, cursor, acc; // sort keys, cub temp, kernel scratch

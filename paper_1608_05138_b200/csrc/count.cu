@@ -44,10 +44,13 @@ constexpr u64 kSmallWedges = 512;    // small-top threshold (<= half the slots)
 constexpr int kBigThreads = 1024;    // block per big top (dense windows), one block per SM
 constexpr int kBigBlocksPerSM = 1;
 constexpr int kMidThreads = 1024;    // block per mid top (hash), one block per SM
+constexpr int kSmidThreads = 256;    // block per small-mid top (hash), four blocks per SM
 constexpr int kWindow = 32768;       // dense W window words (u32, or 2 x u16) in shared memory
 constexpr int kMidLog = 15;
 constexpr u32 kMidSlots = 1u << kMidLog; // mid tops: block hash, u32 keys + u16 counts (192 KB)
 constexpr u64 kMidWedges = kMidSlots / 2; // mid-top threshold (<= half the hash slots)
+constexpr int kSmidLog = 13;
+constexpr u64 kSmidWedges = (1u << kSmidLog) / 2; // small-mid threshold
 
 constexpr u32 kEmpty = 0xffffffffu;
 
@@ -707,13 +710,36 @@ __host__ __device__ inline u64 big_scratch_words(u32 cap) { return 10ull * cap +
 // W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
 // or an open-addressing hash over all c < a (mid tops, HASH).  Hash keys are
 // u32 (kEmpty = free), counts u16 packed two per word.
-__device__ __forceinline__ u32 mid_slot(u32 c) { return (c * 0x9E3779B1u) >> (32 - kMidLog); }
+// cycle block kernel kinds: 0 dense windows (big tops), 1 block hash with
+// 2^15 slots (mid tops), 2 block hash with 2^13 slots and four 256-thread
+// blocks per SM (small-mid tops: their fixed per-top latency overlaps)
+template <int KIND> struct Cyc;
+template <> struct Cyc<0> {
+    static constexpr bool HASH = false;
+    static constexpr int THREADS = kBigThreads, MINB = kBigBlocksPerSM;
+    static constexpr u32 LOG = 0, WORDS = kWindow, META = 7168;
+};
+template <> struct Cyc<1> {
+    static constexpr bool HASH = true;
+    static constexpr int THREADS = kMidThreads, MINB = 1;
+    static constexpr u32 LOG = kMidLog, WORDS = (1u << kMidLog) * 3 / 2, META = 2048;
+};
+template <> struct Cyc<2> {
+    static constexpr bool HASH = true;
+    static constexpr int THREADS = kSmidThreads, MINB = 4;
+    static constexpr u32 LOG = kSmidLog, WORDS = (1u << kSmidLog) * 3 / 2, META = 256;
+};
+template <int KIND> __host__ __device__ constexpr u32 cyc_smem_words() {
+    return Cyc<KIND>::WORDS + 3 * Cyc<KIND>::META + 1;
+}
 
-template <bool HASH>
+
+template <int KIND>
 __device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, bool half) {
-    if (HASH) {
+    constexpr u32 NS = 1u << Cyc<KIND>::LOG;
+    if (Cyc<KIND>::HASH) {
         u32* keys = W;
-        u32 h = mid_slot(c);
+        u32 h = (c * 0x9E3779B1u) >> (32 - Cyc<KIND>::LOG);
         for (;;) {
             const u32 k = keys[h];
             if (k == c) break;
@@ -721,19 +747,20 @@ __device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, bool half) {
                 const u32 prev = atomicCAS(&keys[h], kEmpty, c);
                 if (prev == kEmpty || prev == c) break;
             }
-            h = (h + 1) & (kMidSlots - 1);
+            h = (h + 1) & (NS - 1);
         }
-        atomicAdd(&W[kMidSlots + (h >> 1)], 1u << ((h & 1) << 4));
+        atomicAdd(&W[NS + (h >> 1)], 1u << ((h & 1) << 4));
     } else {
         w_inc(W, c - lo, half);
     }
 }
-template <bool HASH>
+template <int KIND>
 __device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, bool half) {
-    if (HASH) {
-        u32 h = mid_slot(c);
-        while (W[h] != c) h = (h + 1) & (kMidSlots - 1);
-        return (W[kMidSlots + (h >> 1)] >> ((h & 1) << 4)) & 0xffffu;
+    constexpr u32 NS = 1u << Cyc<KIND>::LOG;
+    if (Cyc<KIND>::HASH) {
+        u32 h = (c * 0x9E3779B1u) >> (32 - Cyc<KIND>::LOG);
+        while (W[h] != c) h = (h + 1) & (NS - 1);
+        return (W[NS + (h >> 1)] >> ((h & 1) << 4)) & 0xffffu;
     } else {
         return w_get(W, c - lo, half);
     }
@@ -748,13 +775,13 @@ __device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, bool half) 
         W[ci] = 0;
 }
 
-template <bool HASH, int PASS>
+template <int KIND, int PASS>
 __device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, bool half, i64* __restrict__ slot_acc, u64 slot,
                                          u64& val) {
     if (PASS == 0) {
-        tab_inc<HASH>(W, cv, lo, half);
+        tab_inc<KIND>(W, cv, lo, half);
     } else if (PASS == 1) {
-        const u32 v = tab_get<HASH>(W, cv, lo, half) - 1u;
+        const u32 v = tab_get<KIND>(W, cv, lo, half) - 1u;
         if (v) atomic_add_i64(&slot_acc[slot], (i64)v);
         val = v;
     } else {
@@ -792,7 +819,7 @@ __device__ __forceinline__ u32 warp_upper_bound(const u32* a, u32 n, u32 x) {
 //   PASS 2: W[c] = 0 (sparse clear of a dense window)
 constexpr int kUnroll = 8; // uniform-path rounds with loads in flight per lane
 
-template <bool HASH, int PASS>
+template <int KIND, int PASS>
 __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,
                                             u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
     const u32 lane = lane_id();
@@ -816,7 +843,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                 for (int u = 0; u < kUnroll; ++u) {
                     if (cv[u] != kEmpty) {
                         u64 v = 0;
-                        wedge_op<HASH, PASS>(W, cv[u], lo, half, slot_acc, sbase + 32u * (r + u), v);
+                        wedge_op<KIND, PASS>(W, cv[u], lo, half, slot_acc, sbase + 32u * (r + u), v);
                         acc += v;
                     }
                 }
@@ -844,7 +871,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             u64 v = 0;
             if (valid) {
                 const u64 slot = (u64)S.rs[q] + (k - opi);
-                wedge_op<HASH, PASS>(W, __ldg(g.adj + slot), lo, half, slot_acc, slot, v);
+                wedge_op<KIND, PASS>(W, __ldg(g.adj + slot), lo, half, slot_acc, slot, v);
             }
             if (PASS == 1) {
                 const u32 off = k - opi;
@@ -863,11 +890,6 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
     }
 }
 
-__host__ __device__ constexpr u32 tab_words(bool hash) { return hash ? kMidSlots + kMidSlots / 2 : (u32)kWindow; }
-__host__ __device__ constexpr int tab_threads(bool hash) { return hash ? kMidThreads : kBigThreads; }
-// runs whose metadata fits in shared memory beside the table (12 B per run)
-__host__ __device__ constexpr u32 meta_cap(bool hash) { return hash ? 2048u : 7168u; }
-__host__ __device__ constexpr u32 smem_words(bool hash) { return tab_words(hash) + 3 * meta_cap(hash) + 1; }
 // wedges per dynamic work grab of one warp: ~8 grabs per warp and pass, at least 512
 __device__ __forceinline__ u32 grab_size(u32 T, u32 nwarps) {
     const u32 g = (T / (nwarps * 8u) + 31u) & ~31u;
@@ -887,7 +909,7 @@ __device__ __forceinline__ u32 grab_size(u32 T, u32 nwarps) {
 // are the full row prefixes N(b) n [0,a), one "window", no cursors.  Credits
 // go to per-adjacency-slot accumulators (consecutive wedges of a run are
 // consecutive slots), folded into edge rows by k_fold_slots.
-template <bool HASH, int PASS>
+template <int KIND, int PASS>
 __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u32 nnz, u32 T, u32* counter, u32* W,
                                           u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
     const u32 grab = grab_size(T, blockDim.x >> 5);
@@ -896,7 +918,7 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
         if (lane_id() == 0) k0 = atomicAdd(counter, grab);
         k0 = __shfl_sync(0xffffffffu, k0, 0);
         if (k0 >= T) break;
-        window_pass<HASH, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, half, abase, slot_acc);
+        window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, half, abase, slot_acc);
     }
 }
 
@@ -904,19 +926,20 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
 __device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..26] mid hash
 #endif
 
-template <bool HASH>
-__global__ void __launch_bounds__(tab_threads(HASH), HASH ? 1 : kBigBlocksPerSM)
+template <int KIND>
+__global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
-    constexpr int THREADS = tab_threads(HASH);
-    constexpr u32 kWords = tab_words(HASH);
+    constexpr bool HASH = Cyc<KIND>::HASH;
+    constexpr int THREADS = Cyc<KIND>::THREADS;
+    constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
     extern __shared__ u32 W[]; // kWords table words, then the run metadata
     __shared__ unsigned long long s_idx;
     __shared__ u32 s_next, s_work[3];
     BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
-    const RunMeta Msm{W + kWords, W + kWords + meta_cap(HASH) + 1, W + kWords + 2 * meta_cap(HASH) + 1};
+    const RunMeta Msm{W + kWords, W + kWords + kMeta + 1, W + kWords + 2 * kMeta + 1};
     const RunMeta Mgl{S.pre, S.rs, S.rj};
-    for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
+    for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
 #ifdef GL_CYCLE_PROF
     // make prof: per-phase clock64 totals (thread 0, between barriers): 0 setup,
     // 6 gallop, 1 scan, 2 compaction, 3 pass 0, 4 pass 1, 7 clear, 5 grab;
@@ -1001,7 +1024,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             GL_PROF_MARK(1);
             GL_PROF_ADD(8, 1);
             GL_PROF_ADD(9, T);
-            const RunMeta M = nnz <= meta_cap(HASH) ? Msm : Mgl;
+            const RunMeta M = nnz <= kMeta ? Msm : Mgl;
             if (my_runs) {
                 u32 q = (u32)(mine >> 32), w = (u32)mine;
                 for (u32 j = threadIdx.x; j < nb; j += THREADS) {
@@ -1022,29 +1045,29 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if (T) {
                 const bool bulk_clear = HASH || T > kWords / 8;
                 {
-                    if (nnz <= meta_cap(HASH)) // shared-memory metadata: LDS in the walk
-                        grab_pass<HASH, 0>(g, Msm, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
+                    if (nnz <= kMeta) // shared-memory metadata: LDS in the walk
+                        grab_pass<KIND, 0>(g, Msm, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
                     else
-                        grab_pass<HASH, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
                 }
                 __syncthreads();
                 GL_PROF_MARK(3);
                 {
-                    if (nnz <= meta_cap(HASH))
-                        grab_pass<HASH, 1>(g, Msm, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
+                    if (nnz <= kMeta)
+                        grab_pass<KIND, 1>(g, Msm, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
                     else
-                        grab_pass<HASH, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
                 }
                 __syncthreads();
                 GL_PROF_MARK(4);
                 if (bulk_clear) {
                     const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
-                    for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kMidSlots) ? kEmpty : 0u;
+                    for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
                 } else if (!HASH) {
-                    if (nnz <= meta_cap(HASH))
-                        grab_pass<HASH, 2>(g, Msm, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+                    if (nnz <= kMeta)
+                        grab_pass<KIND, 2>(g, Msm, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
                     else
-                        grab_pass<HASH, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
                 }
             }
             GL_PROF_SYNC_MARK(7);
@@ -1057,7 +1080,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     }
 #ifdef GL_CYCLE_PROF
     if (threadIdx.x == 0)
-        for (int k = 0; k < 11; ++k) atomicAdd(&g_cycle_prof[k + (HASH ? 16 : 0)], pf[k]);
+        for (int k = 0; k < 11; ++k) atomicAdd(&g_cycle_prof[k + (KIND ? 16 : 0)], pf[k]);
 #endif
 }
 
@@ -1219,16 +1242,19 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
 // windows), mid (> kSmallWedges, block hash), small (warp hash)
 __global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u32* __restrict__ keys,
                            unsigned long long* __restrict__ n_big, unsigned long long* __restrict__ n_mid,
-                           unsigned long long* __restrict__ n_small) {
-    unsigned long long lb = 0, lm = 0, ls = 0;
+                           unsigned long long* __restrict__ n_smid, unsigned long long* __restrict__ n_small) {
+    unsigned long long lb = 0, lm = 0, lq = 0, ls = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         u64 w = wpre[g.loff[a + 1]] - wpre[g.loff[a]];
         u32 cls = 0; // exact class boundaries: class above the log cost
         if (w > kMidWedges) {
             ++lb;
+            cls = 4;
+        } else if (w > kSmidWedges) {
+            ++lm;
             cls = 3;
         } else if (w > kSmallWedges) {
-            ++lm;
+            ++lq;
             cls = 2;
         } else if (w) {
             ++ls;
@@ -1238,6 +1264,7 @@ __global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u32* __rest
     }
     if (lb) atomicAdd(n_big, lb);
     if (lm) atomicAdd(n_mid, lm);
+    if (lq) atomicAdd(n_smid, lq);
     if (ls) atomicAdd(n_small, ls);
 }
 
@@ -1423,51 +1450,47 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
             k_top_keys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,
-                                                           counters + 11);
+                                                           counters + 16, counters + 11);
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
             const u64 nbig = read_dev<unsigned long long>(counters + 10, s);
             const u64 nmid = read_dev<unsigned long long>(counters + 15, s);
+            const u64 nsmid = read_dev<unsigned long long>(counters + 16, s);
             const u64 nsmall = read_dev<unsigned long long>(counters + 11, s);
             cs.work[2] = 12 * read_dev(cs.wpre.as<u64>() + m, s) / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mymid = rank_share(nmid, rank, world);
+            const u64 mysmid = rank_share(nsmid, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
             u32* lbig = iin;
-            u32* lmid = iin + mybig;
-            u32* lsmall = lmid + mymid;
-            if (mybig || mymid) {
+            u32* lmid = lbig + mybig;
+            u32* lsmid = lmid + mymid;
+            u32* lsmall = lsmid + mysmid;
+            if (mybig || mymid || mysmid) {
                 if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
                 const u32 cap = (g.dmax + 3) & ~1u;
-                const unsigned blocks = (unsigned)sms * 2; // 1 big or 2 mid blocks per SM
+                const unsigned blocks = (unsigned)sms * 4; // up to 4 small-mid blocks per SM
                 cs.cursor.alloc((u64)blocks * ((big_scratch_words(cap) + 1) & ~1ull) * sizeof(u32));
-                if (mybig) {
-                    k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, lbig);
+                auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
+                    constexpr int K = decltype(kind)::value;
+                    k_take_rank<<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
-                    const size_t smem = (size_t)smem_words(false) * sizeof(u32);
-                    GL_CUDA(cudaFuncSetAttribute(k_cycle_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
+                    GL_CUDA(cudaFuncSetAttribute(k_cycle_block<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
-                    k_cycle_block<false><<<(unsigned)sms * kBigBlocksPerSM, kBigThreads, smem, s>>>(g, lbig, mybig, counters + 1,
-                                                                          cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
+                    k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s>>>(
+                        g, list, count, queue, cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
-                }
-                if (mymid) {
-                    k_take_rank<<<grid1d(mymid, 256, sms), 256, 0, s>>>(iout, nbig, nmid, rank, world, lmid);
-                    GL_LAUNCH_CHECK();
-                    const size_t smem = (size_t)smem_words(true) * sizeof(u32);
-                    GL_CUDA(cudaFuncSetAttribute(k_cycle_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem));
-                    k_cycle_block<true><<<(unsigned)sms, kMidThreads, smem, s>>>(g, lmid, mymid, counters + 4,
-                                                                         cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
-                    GL_LAUNCH_CHECK();
-                    cs.launches += 2;
-                }
+                };
+                if (mybig) launch(std::integral_constant<int, 0>{}, lbig, mybig, 0, nbig, counters + 1);
+                if (mymid) launch(std::integral_constant<int, 1>{}, lmid, mymid, nbig, nmid, counters + 4);
+                if (mysmid) launch(std::integral_constant<int, 2>{}, lsmid, mysmid, nbig + nmid, nsmid, counters + 7);
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmid, nsmall, rank, world, lsmall);
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmid + nsmid, nsmall, rank, world, lsmall);
                 GL_LAUNCH_CHECK();
                 const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
                 GL_CUDA(cudaFuncSetAttribute(k_cycle_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

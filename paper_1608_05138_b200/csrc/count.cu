@@ -890,10 +890,14 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
     }
 }
 
-// wedges per dynamic work grab of one warp: ~8 grabs per warp and pass, at least 512
-__device__ __forceinline__ u32 grab_size(u32 T, u32 nwarps) {
-    const u32 g = (T / (nwarps * 8u) + 31u) & ~31u;
-    return g > 512u ? g : 512u;
+// Guided self-scheduling of a window pass: a warp grabs about 1/(2*nwarps) of
+// the wedges still unclaimed (at most 8192, at least 64), so the grabs shrink
+// towards the end of the pass and the block's barrier waits for a short tail.
+__device__ __forceinline__ u32 grab_size(u32 remaining, u32 nwarps) {
+    u32 g = remaining / (2u * nwarps);
+    g = g < 8192u ? g : 8192u;
+    g = (g + 31u) & ~31u;
+    return g > 64u ? g : 64u;
 }
 
 // Mid and big tops: one block per top a (persistent blocks, atomic queue over
@@ -912,11 +916,16 @@ __device__ __forceinline__ u32 grab_size(u32 T, u32 nwarps) {
 template <int KIND, int PASS>
 __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u32 nnz, u32 T, u32* counter, u32* W,
                                           u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
-    const u32 grab = grab_size(T, blockDim.x >> 5);
+    const u32 nwarps = blockDim.x >> 5;
     for (;;) {
-        u32 k0 = 0;
-        if (lane_id() == 0) k0 = atomicAdd(counter, grab);
+        u32 k0 = 0, grab = 0;
+        if (lane_id() == 0) {
+            const u32 seen = *(volatile u32*)counter;
+            grab = grab_size(seen < T ? T - seen : 0u, nwarps);
+            k0 = atomicAdd(counter, grab);
+        }
         k0 = __shfl_sync(0xffffffffu, k0, 0);
+        grab = __shfl_sync(0xffffffffu, grab, 0);
         if (k0 >= T) break;
         window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, half, abase, slot_acc);
     }

@@ -70,6 +70,10 @@ int gl_load_edge_list(const char *text, size_t len, uint64_t **pairs, uint64_t *
 /* load_edge_list_file (graph.hpp:39; graph.cpp:87-91). */
 int gl_load_edge_list_file(const char *path, uint64_t **pairs, uint64_t *count);
 void gl_free(void *p);
+/* Device memory freed by gl_graph_free is cached per device for the next
+ * graph (no reference counterpart: the reference is host-only); this returns
+ * the cache to the driver. */
+int gl_trim_device_cache(void);
 
 /* Deterministic synthetic generators (SPEC cli "built-in deterministic
  * generator"); host output, 2*count labels.  RMAT uses Graph500 quadrant

@@ -113,6 +113,10 @@ uint64_t gl_last_error_line(void) { return t_line; }
 const char* gl_version(void) { return "graphlet_b200 0.1 (sm_100a)"; }
 void gl_free(void* p) { std::free(p); }
 
+int gl_trim_device_cache(void) {
+    return guarded([&] { gl::pool_trim(); });
+}
+
 int gl_load_edge_list(const char* text, size_t len, uint64_t** pairs, uint64_t* count) {
     return guarded([&] {
         if (!text && len) throw gl::invalid_argument("null text");

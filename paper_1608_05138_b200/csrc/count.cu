@@ -28,6 +28,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <type_traits>
 #include <cstring>
 #include <vector>
@@ -707,6 +710,7 @@ __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
 }
 __host__ __device__ inline u64 big_scratch_words(u32 cap) { return 10ull * cap + 8; }
 
+
 // W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
 // or an open-addressing hash over all c < a (mid tops, HASH).  Hash keys are
 // u32 (kEmpty = free), counts u16 packed two per word.
@@ -1006,8 +1010,10 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         // next window's cursors (pointer swap, no extra pass)
         u32* cur = S.cur;
         u32* nxt = S.hpos;
-        for (u32 lo = s_next; lo < a; lo = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a)) {
+        u32 win = 0;
+        for (u32 lo = s_next; lo < a; lo = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a), ++win) {
             const u32 hi = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a);
+
             // run ends; runs are ordered thread-major (thread t owns b = t + i*THREADS,
             // coalesced), so one block scan of per-thread (runs, wedges) places them
             u32 my_runs = 0, my_wedges = 0;
@@ -1317,6 +1323,15 @@ void dev_sort_desc(DevBuf& tmp, u32* keys_in, u32* keys_out, u32* ids_in, u32* i
                                                       (int64_t)n, 0, (int)kKeyBits, s));
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size)
+template <typename K> void smem_attr(K* kernel, size_t smem, int device) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, size_t>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({reinterpret_cast<const void*>(kernel), device, smem}).second)
+        GL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
 template <typename T> T read_dev(const T* p, cudaStream_t s) {
     T h{};
     GL_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -1388,13 +1403,16 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* iout = iin + (n + 1);
             k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17, counters + 18,
                                                         counters + 19);
+            k_umax<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 14));
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
-            cs.launches += 2 + 10;
-            const u64 nbig = read_dev<unsigned long long>(counters + 12, s);
-            const u64 nsmall = read_dev<unsigned long long>(counters + 13, s);
-            cs.s1 = read_dev<unsigned long long>(counters + 17, s);
+            cs.launches += 3 + 10;
+            u64 hc[24]; // one host round trip for all class counts and bounds
+            GL_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
+            GL_CUDA(cudaStreamSynchronize(s));
+            const u64 nbig = hc[12], nsmall = hc[13];
+            cs.s1 = hc[17];
             cs.work[0] = 4 * cs.s1 / (u64)world; // adjacency bytes streamed by the intersections
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
@@ -1403,13 +1421,11 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             cs.items3b.alloc((mybig + 1) * sizeof(u32));
             cs.items3s.alloc((mysmall + 1) * sizeof(u32));
             if (mybig) {
-                const u64 s1max = read_dev<unsigned long long>(counters + 18, s);
+                const u64 s1max = hc[18];
                 k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, cs.items3b.as<u32>());
                 GL_LAUNCH_CHECK();
                 const unsigned blocks = (unsigned)sms * 2;
-                k_umax<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 14));
-                GL_LAUNCH_CHECK();
-                const u32 kmax = (u32)read_dev<unsigned long long>(counters + 14, s);
+                const u32 kmax = (u32)(hc[14] & 0xffffffffu);
                 if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
                 cs.h_gstride = 0;
                 if (kmax > (u32)kHSmemMax) {
@@ -1418,20 +1434,19 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 }
                 const u64 hcap = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
                 cs.hlist.alloc((u64)blocks * hcap * sizeof(uint2));
-                // persistent H-edge records for the sums pass, up to ~40% of free memory
-                {
-                    const u64 bound = read_dev<unsigned long long>(counters + 19, s);
+                // persistent H-edge records for the sums pass: sized once per graph from
+                // the bound sum_a min(C(k,2), s1(a)), at most ~40% of the free memory
+                if (!cs.tl_sized) {
                     size_t fr = 0, tot = 0;
                     GL_CUDA(cudaMemGetInfo(&fr, &tot));
-                    const u64 cap = std::min<u64>(bound, (u64)(0.4 * (double)fr) / sizeof(uint2));
-                    cs.tl_cap = cap;
-                    cs.tlist.alloc((cap + 1) * sizeof(uint2));
-                    cs.tl_base.alloc((mybig + 1) * sizeof(u64));
-                    cs.tl_n.alloc((mybig + 1) * sizeof(u32));
+                    cs.tl_cap = std::min<u64>(hc[19] / (u64)world + 1, (u64)(0.4 * (double)fr) / sizeof(uint2));
+                    cs.tl_sized = true;
                 }
+                cs.tlist.alloc((cs.tl_cap + 1) * sizeof(uint2));
+                cs.tl_base.alloc((mybig + 1) * sizeof(u64));
+                cs.tl_n.alloc((mybig + 1) * sizeof(u32));
                 const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassCount) * sizeof(u32);
-                GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
+                smem_attr(k_hpass_block<kHPassCount>, smem, gr.device);
                 const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
                 k_hpass_block<kHPassCount><<<blocks, kHBlockThreads, smem, s>>>(
                     g, cs.items3b.as<u32>(), mybig, counters + 0, cs.t.as<u32>(), d_partials,
@@ -1463,11 +1478,11 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
-            const u64 nbig = read_dev<unsigned long long>(counters + 10, s);
-            const u64 nmid = read_dev<unsigned long long>(counters + 15, s);
-            const u64 nsmid = read_dev<unsigned long long>(counters + 16, s);
-            const u64 nsmall = read_dev<unsigned long long>(counters + 11, s);
-            cs.work[2] = 12 * read_dev(cs.wpre.as<u64>() + m, s) / (u64)world; // 4 B c id + 8 B slot credit per wedge
+            u64 cc[24];
+            GL_CUDA(cudaMemcpyAsync(cc, counters, sizeof(cc), cudaMemcpyDeviceToHost, s));
+            const u64 wtot = read_dev(cs.wpre.as<u64>() + m, s);
+            const u64 nbig = cc[10], nmid = cc[15], nsmid = cc[16], nsmall = cc[11];
+            cs.work[2] = 12 * wtot / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mymid = rank_share(nmid, rank, world);
@@ -1479,18 +1494,24 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* lsmall = lsmid + mysmid;
             if (mybig || mymid || mysmid) {
                 if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
-                const u32 cap = (g.dmax + 3) & ~1u;
-                const unsigned blocks = (unsigned)sms * 4; // up to 4 small-mid blocks per SM
-                cs.cursor.alloc((u64)blocks * ((big_scratch_words(cap) + 1) & ~1ull) * sizeof(u32));
+                // per-block scratch: big tops need dmax + 2 entries, hash tops at most
+                // their wedge bound (nb <= wedges)
+                const u32 cap_big = (g.dmax + 3) & ~1u;
+                const u32 cap_hash = std::min<u32>(cap_big, (u32)kMidWedges + 2);
+                const u64 w_big = (big_scratch_words(cap_big) + 1) & ~1ull;
+                const u64 w_hash = (big_scratch_words(cap_hash) + 1) & ~1ull;
+                if (mybig) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
+                if (mymid || mysmid) cs.cursor2.alloc((u64)sms * 4 * w_hash * sizeof(u32));
                 auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
                     constexpr int K = decltype(kind)::value;
+                    const u32 cap = K == 0 ? cap_big : cap_hash;
+                    u32* scratch = K == 0 ? cs.cursor.as<u32>() : cs.cursor2.as<u32>();
                     k_take_rank<<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
-                    GL_CUDA(cudaFuncSetAttribute(k_cycle_block<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem));
+                    smem_attr(k_cycle_block<K>, smem, gr.device);
                     k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s>>>(
-                        g, list, count, queue, cs.slots.as<i64>(), cs.cursor.as<u32>(), cap);
+                        g, list, count, queue, cs.slots.as<i64>(), scratch, cap);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };
@@ -1502,7 +1523,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmid + nsmid, nsmall, rank, world, lsmall);
                 GL_LAUNCH_CHECK();
                 const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
-                GL_CUDA(cudaFuncSetAttribute(k_cycle_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                smem_attr(k_cycle_small, smem, gr.device);
                 k_cycle_small<<<(unsigned)sms * 3, kCycleSmallWarps * 32, smem, s>>>(
                     g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, cs.slots.as<i64>());
                 GL_LAUNCH_CHECK();
@@ -1536,8 +1557,7 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     if (g.m && cs.n_items3b) {
         const unsigned blocks = (unsigned)sms * 2;
         const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassSums) * sizeof(u32);
-        GL_CUDA(cudaFuncSetAttribute(k_hpass_block<kHPassSums>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+        smem_attr(k_hpass_block<kHPassSums>, smem, gr.device);
         const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
         k_hpass_block<kHPassSums><<<blocks, kHBlockThreads, smem, s>>>(
             g, cs.items3b.as<u32>(), cs.n_items3b, counters + 5, cs.t.as<u32>(), d_partials,

@@ -34,16 +34,25 @@ struct DevGraph {
     u64* label = nullptr;
 };
 
-// RAII device buffer
+// Process-wide caching allocator (host.cpp): freed blocks are kept per device
+// and handed out again for requests of at most their size and at least half
+// of it, so building and counting a new graph every step does not pay
+// cudaMalloc / cudaFree of the multi-GB working set each time.
+void* pool_alloc(size_t bytes, int device, size_t* got);
+void pool_free(void* p, size_t bytes, int device);
+void pool_trim();
+
+// RAII device buffer (pool-backed)
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    int dev = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { reset(); }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, bytes, dev);
         p = nullptr;
         bytes = 0;
     }
@@ -51,8 +60,8 @@ struct DevBuf {
         if (b <= bytes && p) return;
         reset();
         if (b == 0) b = 16;
-        GL_CUDA(cudaMalloc(&p, b));
-        bytes = b;
+        GL_CUDA(cudaGetDevice(&dev));
+        p = pool_alloc(b, dev, &bytes);
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
 };
@@ -66,9 +75,10 @@ struct CountState {
     DevBuf hlist;    // per-block H-edge lists of the clique pass
     DevBuf tlist, tl_base, tl_n; // persistent H-edge records for the triangle-sum pass
     u64 tl_cap = 0;
+    bool tl_sized = false;
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3b; // work lists
-    DevBuf keys, tmp, scratch, cursor, acc; // sort keys, cub temp, kernel scratch
+    DevBuf keys, tmp, scratch, cursor, cursor2, acc; // sort keys, cub temp, kernel scratch
     u64 n_items2 = 0, n_items3s = 0, n_items3b = 0;
     u64 shard_begin = 0, shard_end = 0;
     bool have_micro = false;

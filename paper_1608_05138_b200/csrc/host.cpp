@@ -5,12 +5,86 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <map>
+#include <mutex>
 #include <unordered_set>
 #include <vector>
 
 #include "graph.cuh"
 
 namespace gl {
+
+// ------------------------------------------------------------------ device memory pool
+
+namespace {
+struct Pool {
+    std::mutex mu;
+    std::multimap<size_t, std::pair<int, void*>> cached; // size -> (device, ptr)
+    size_t cached_bytes = 0;
+};
+Pool& pool() {
+    static Pool* p = new Pool; // never destroyed: blocks may be freed during static teardown
+    return *p;
+}
+constexpr size_t kPoolMaxCached = 96ull << 30;
+} // namespace
+
+void* pool_alloc(size_t bytes, int device, size_t* got) {
+    bytes = (bytes + 255) & ~size_t(255);
+    Pool& P = pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (auto it = P.cached.lower_bound(bytes); it != P.cached.end() && it->first <= 2 * bytes; ++it) {
+            if (it->second.first != device) continue;
+            void* p = it->second.second;
+            *got = it->first;
+            P.cached_bytes -= it->first;
+            P.cached.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) { // give the cache back and retry once
+        cudaGetLastError();
+        pool_trim();
+        e = cudaMalloc(&p, bytes);
+    }
+    cuda_check(e, "cudaMalloc", __FILE__, __LINE__);
+    *got = bytes;
+    return p;
+}
+
+void pool_free(void* p, size_t bytes, int device) {
+    Pool& P = pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        if (P.cached_bytes + bytes <= kPoolMaxCached) {
+            P.cached.emplace(bytes, std::make_pair(device, p));
+            P.cached_bytes += bytes;
+            return;
+        }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaFree(p);
+    cudaSetDevice(cur);
+}
+
+void pool_trim() {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : P.cached) {
+        cudaSetDevice(kv.second.first);
+        cudaFree(kv.second.second);
+    }
+    cudaSetDevice(cur);
+    P.cached.clear();
+    P.cached_bytes = 0;
+}
 
 // ------------------------------------------------------------------ parser
 

@@ -119,21 +119,28 @@ __device__ __forceinline__ u64 warp_sum_u64(u64 v) {
 
 __device__ __forceinline__ u64 u_begin(const DevGraph& g, u32 x) { return g.off[x] + g.lcnt[x]; }
 
-constexpr u32 kBloomLog = 16, kBloomWords = (1u << kBloomLog) / 32; // 8 KB member filter
-__device__ __forceinline__ u32 bloom_bit(u32 y) { return (y * 0x2545F491u) >> (32 - kBloomLog); }
+// member filter of the block H-pass: 2^BLOG bits (8 KB for large k, 1 KB for k <= 128)
+template <int BLOG> __device__ __forceinline__ u32 bloom_bit(u32 y) { return (y * 0x2545F491u) >> (32 - BLOG); }
+template <int BLOG> __host__ __device__ constexpr u32 bloom_words() { return (1u << BLOG) / 32; }
+// block H-pass configurations: k > 128 (512 threads, two blocks per SM) and
+// 32 < k <= 128 (128 threads, eight blocks per SM: the fixed per-vertex
+// latency of the many small vertices overlaps across blocks)
+template <int KMAX> struct HCfg;
+template <> struct HCfg<768> { static constexpr int THREADS = 512, MINB = 2, BLOG = 16; };
+template <> struct HCfg<128> { static constexpr int THREADS = 128, MINB = 8, BLOG = 13; };
 
 __device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 2k, >= 64 (Bloom filters the misses)
     u32 l = 32 - __clz(2 * k - 1);
     return l < 6 ? 6 : l;
 }
-__host__ __device__ inline u64 hpass_ws_words(u32 k, int mode) {
+__host__ __device__ inline u64 hpass_ws_words(u32 k, int mode, u32 bloom_w) {
     u32 l = 6;
     while ((1u << l) < 2 * k) ++l;
     const u64 H = 1ull << l;
     const u64 W = (k + 31) / 32;
-    const u64 body = mode == 0 ? 2ull * k + (u64)k * W  // xs, tri, rows
+    const u64 body = mode == 0 ? 2ull * k + (u64)k * (W | 1)  // xs, tri, rows (odd stride)
                                : 4ull * k + 2;          // xs, ta, acc (u64, aligned)
-    return body + 2 + H + H / 2 + kBloomWords;
+    return body + 2 + H + H / 2 + bloom_w;
 }
 
 __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
@@ -310,7 +317,7 @@ struct TriList {
 };
 constexpr u64 kNoList = ~0ull;
 
-template <int MODE, typename Cand>
+template <int MODE, int BLOG, typename Cand>
 __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
                                              Cand* cbuf, uint2* hlist, u32& s_nh, u32& s_mi, u32 a, u64 ub, u32 k,
                                              u32 W, u32 hl, u32 H, const TriList& TL, u64 idx, u64& s_base) {
@@ -358,9 +365,12 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     u32* rows = tri + k;                    // kHPassCount
     u32* ta = xs + k;                       // kHPassSums
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
-    const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * W : ((2ull * k + 1) & ~1ull) + 2ull * k;
+    // bitmap rows use an odd word stride RS so that the rows of different
+    // members fall in different banks (phase 2 reads two arbitrary rows)
+    const u32 RS = W | 1u;
+    const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * RS : ((2ull * k + 1) & ~1ull) + 2ull * k;
     u32* bloom = ws + body;
-    u32* hkey = bloom + kBloomWords;
+    u32* hkey = bloom + bloom_words<BLOG>();
     unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
     for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
         xs[i] = g.adj[ub + i];
@@ -372,16 +382,16 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         }
     }
     if (MODE == kHPassCount)
-        for (u64 w = threadIdx.x; w < (u64)k * W; w += blockDim.x) rows[w] = 0;
+        for (u64 w = threadIdx.x; w < (u64)k * RS; w += blockDim.x) rows[w] = 0;
     for (u32 h = threadIdx.x; h < H; h += blockDim.x) hkey[h] = kEmpty;
-    for (u32 w = threadIdx.x; w < kBloomWords; w += blockDim.x) bloom[w] = 0;
+    for (u32 w = threadIdx.x; w < bloom_words<BLOG>(); w += blockDim.x) bloom[w] = 0;
     __syncthreads();
     for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
         const u32 x = xs[i];
         u32 h = (x * 0x9E3779B1u) >> (32 - hl);
         while (atomicCAS(&hkey[h], kEmpty, x) != kEmpty) h = (h + 1) & (H - 1);
         hval[h] = (unsigned short)i;
-        const u32 bb = bloom_bit(x);
+        const u32 bb = bloom_bit<BLOG>(x);
         atomicOr(&bloom[bb >> 5], 1u << (bb & 31));
     }
     __syncthreads();
@@ -409,7 +419,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
             u32 cand = 0;
 #pragma unroll
             for (int u = 0; u < kHUnroll; ++u) {
-                const u32 bb = bloom_bit(yv[u]);
+                const u32 bb = bloom_bit<BLOG>(yv[u]);
                 if (yv[u] <= xmax && ((bloom[bb >> 5] >> (bb & 31)) & 1u)) cand |= 1u << u; // kEmpty > xmax
             }
             const u32 c = __popc(cand);
@@ -461,8 +471,8 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
                 }
                 if (MODE == kHPassCount) {
                     if (hit) {
-                        atomicOr(&rows[(u64)i * W + (j >> 5)], 1u << (j & 31));
-                        atomicOr(&rows[(u64)j * W + (i >> 5)], 1u << (i & 31));
+                        atomicOr(&rows[(u64)i * RS + (j >> 5)], 1u << (j & 31));
+                        atomicOr(&rows[(u64)j * RS + (i >> 5)], 1u << (i & 31));
                     }
                     const unsigned bal = __ballot_sync(0xffffffffu, hit);
                     if (bal) {
@@ -505,8 +515,8 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
             const uint2 he = hlist[h];
             if (tb != kNoList) TL.rec[tb + h] = he;
             const u32 i = he.x & 0xffffu, j = he.x >> 16;
-            const u32* ri = rows + (u64)i * W;
-            const u32* rj = rows + (u64)j * W;
+            const u32* ri = rows + (u64)i * RS;
+            const u32* rj = rows + (u64)j * RS;
             u32 c = 0;
             for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
             atomicAdd(&t[he.y], 1u);
@@ -520,7 +530,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // phase 3: edges (a, x_i)
         for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
             u32 deg = 0;
-            const u32* ri = rows + (u64)i * W;
+            const u32* ri = rows + (u64)i * RS;
             for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
             const u32 e = g.eid[ub + i];
             if (deg) atomicAdd(&t[e], deg);
@@ -532,11 +542,12 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kHBlockThreads, 2)
+template <int MODE, int KMAX>
+__global__ void __launch_bounds__(HCfg<KMAX>::THREADS, HCfg<KMAX>::MINB)
 k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
               uint2* __restrict__ hlist_all, u64 hcap, TriList TL) {
+    constexpr int BLOG = HCfg<KMAX>::BLOG;
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
     __shared__ u64 s_base;
@@ -545,7 +556,7 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     // pass keeps offsets only (its bitmap rows need the shared memory) and
     // re-reads y from L1
     using Cand = typename std::conditional<MODE == kHPassSums, uint2, unsigned short>::type;
-    __shared__ Cand s_cbuf[kHBlockThreads / 32][32 * kHUnroll];
+    __shared__ Cand s_cbuf[HCfg<KMAX>::THREADS / 32][32 * kHUnroll];
     const u32 lane = lane_id();
     Cand* cbuf = s_cbuf[threadIdx.x >> 5];
     uint2* hlist = MODE == kHPassCount ? hlist_all + (u64)blockIdx.x * hcap : nullptr;
@@ -565,16 +576,15 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 W = (k + 31) >> 5;
         const u32 hl = hp_log(k), H = 1u << hl;
         if (MODE == kHPassSums) // one generic-pointer copy measured faster for the lighter sums pass
-            hpass_vertex<MODE>(g, t, part, k <= (u32)kHSmemMax ? smem : gscratch + (u64)blockIdx.x * gstride, cbuf,
-                               hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
-        else if (k <= (u32)kHSmemMax)
-            hpass_vertex<MODE>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
+            hpass_vertex<MODE, BLOG>(g, t, part, k <= (u32)KMAX ? smem : gscratch + (u64)blockIdx.x * gstride,
+                                     cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
+        else if (k <= (u32)KMAX)
+            hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
         else
-            hpass_vertex<MODE>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a, ub,
-                               k, W, hl, H, TL, idx, s_base);
+            hpass_vertex<MODE, BLOG>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a,
+                                     ub, k, W, hl, H, TL, idx, s_base);
     }
 }
-
 
 // ------------------------------------------------------------------ cycles
 
@@ -1218,11 +1228,12 @@ __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     }
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
-__global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* __restrict__ cnt,
+// classes: 3 = k > 128 (large block), 2 = 32 < k <= 128 (small block), 1 = 2 <= k <= 32 (warp)
+__global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* __restrict__ n_large,
+                        unsigned long long* __restrict__ n_medium, unsigned long long* __restrict__ n_small,
                         unsigned long long* __restrict__ s1_total, unsigned long long* __restrict__ s1_max,
                         unsigned long long* __restrict__ hedge_bound) {
-    unsigned long long mx = 0, hb = 0;
-    unsigned long long lb = 0, ls = 0, st = 0;
+    unsigned long long mx = 0, hb = 0, ll = 0, lm = 0, ls = 0, st = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         const u64 ub = g.off[a] + g.lcnt[a];
         const u64 k = g.off[a + 1] - ub;
@@ -1234,20 +1245,23 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
                 q += g.off[x + 1] - (g.off[x] + g.lcnt[x]);
             }
             st += q;
-            key = (k > (u64)kHWarpMax ? kClassBit : 0u) | (log_key(q) + 1);
+            u32 cls = 1;
             if (k > (u64)kHWarpMax) {
-                ++lb;
+                cls = k > 128 ? 3 : 2;
+                if (cls == 3) ++ll; else ++lm;
                 mx = q > mx ? q : mx;
                 const u64 pairs = k * (k - 1) / 2;
                 hb += pairs < q ? pairs : q;
             } else {
                 ++ls;
             }
+            key = (cls << 12) | (log_key(q) + 1);
         }
         keys[a] = key;
     }
-    if (lb) atomicAdd(&cnt[0], lb);
-    if (ls) atomicAdd(&cnt[1], ls);
+    if (ll) atomicAdd(n_large, ll);
+    if (lm) atomicAdd(n_medium, lm);
+    if (ls) atomicAdd(n_small, ls);
     if (st) atomicAdd(s1_total, st);
     if (mx) atomicMax(s1_max, mx);
     if (hb) atomicAdd(hedge_bound, hb);
@@ -1401,8 +1415,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
-            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 17, counters + 18,
-                                                        counters + 19);
+            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 21, counters + 13,
+                                                        counters + 17, counters + 18, counters + 19);
             k_umax<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 14));
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
@@ -1411,29 +1425,31 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u64 hc[24]; // one host round trip for all class counts and bounds
             GL_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
             GL_CUDA(cudaStreamSynchronize(s));
-            const u64 nbig = hc[12], nsmall = hc[13];
+            const u64 nbig = hc[12], nmedk = hc[21], nsmall = hc[13];
             cs.s1 = hc[17];
             cs.work[0] = 4 * cs.s1 / (u64)world; // adjacency bytes streamed by the intersections
             const u64 mybig = rank_share(nbig, rank, world);
+            const u64 mymedk = rank_share(nmedk, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
             cs.n_items3b = mybig;
+            cs.n_items3m = mymedk;
             cs.n_items3s = mysmall;
             cs.items3b.alloc((mybig + 1) * sizeof(u32));
+            cs.items3m.alloc((mymedk + 1) * sizeof(u32));
             cs.items3s.alloc((mysmall + 1) * sizeof(u32));
-            if (mybig) {
+            if (mybig || mymedk) {
                 const u64 s1max = hc[18];
-                k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world, cs.items3b.as<u32>());
-                GL_LAUNCH_CHECK();
-                const unsigned blocks = (unsigned)sms * 2;
                 const u32 kmax = (u32)(hc[14] & 0xffffffffu);
                 if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
+                const unsigned blocks_l = (unsigned)sms * HCfg<768>::MINB, blocks_m = (unsigned)sms * HCfg<128>::MINB;
                 cs.h_gstride = 0;
                 if (kmax > (u32)kHSmemMax) {
-                    cs.h_gstride = (hpass_ws_words(kmax, kHPassCount) + 1) & ~1ull;
-                    cs.scratch.alloc((u64)blocks * cs.h_gstride * sizeof(u32));
+                    cs.h_gstride = (hpass_ws_words(kmax, kHPassCount, bloom_words<HCfg<768>::BLOG>()) + 1) & ~1ull;
+                    cs.scratch.alloc((u64)blocks_l * cs.h_gstride * sizeof(u32));
                 }
-                const u64 hcap = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
-                cs.hlist.alloc((u64)blocks * hcap * sizeof(uint2));
+                const u64 hcap_l = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
+                const u64 hcap_m = std::min<u64>(s1max, 128ull * 127 / 2) + 1;
+                cs.hlist.alloc(std::max<u64>((u64)blocks_l * hcap_l, (u64)blocks_m * hcap_m) * sizeof(uint2));
                 // persistent H-edge records for the sums pass: sized once per graph from
                 // the bound sum_a min(C(k,2), s1(a)), at most ~40% of the free memory
                 if (!cs.tl_sized) {
@@ -1443,19 +1459,41 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     cs.tl_sized = true;
                 }
                 cs.tlist.alloc((cs.tl_cap + 1) * sizeof(uint2));
-                cs.tl_base.alloc((mybig + 1) * sizeof(u64));
-                cs.tl_n.alloc((mybig + 1) * sizeof(u32));
-                const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassCount) * sizeof(u32);
-                smem_attr(k_hpass_block<kHPassCount>, smem, gr.device);
-                const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
-                k_hpass_block<kHPassCount><<<blocks, kHBlockThreads, smem, s>>>(
-                    g, cs.items3b.as<u32>(), mybig, counters + 0, cs.t.as<u32>(), d_partials,
-                    cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, cs.hlist.as<uint2>(), hcap, TL);
-                GL_LAUNCH_CHECK();
-                cs.launches += 3;
+                cs.tl_base.alloc((mybig + mymedk + 1) * sizeof(u64));
+                cs.tl_n.alloc((mybig + mymedk + 1) * sizeof(u32));
+                if (mybig) {
+                    k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world,
+                                                                        cs.items3b.as<u32>());
+                    GL_LAUNCH_CHECK();
+                    const size_t smem =
+                        (size_t)hpass_ws_words(kHSmemMax, kHPassCount, bloom_words<HCfg<768>::BLOG>()) * sizeof(u32);
+                    smem_attr(k_hpass_block<kHPassCount, 768>, smem, gr.device);
+                    const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(),
+                                     cs.tl_n.as<u32>()};
+                    k_hpass_block<kHPassCount, 768><<<blocks_l, HCfg<768>::THREADS, smem, s>>>(
+                        g, cs.items3b.as<u32>(), mybig, counters + 0, cs.t.as<u32>(), d_partials,
+                        cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, cs.hlist.as<uint2>(), hcap_l, TL);
+                    GL_LAUNCH_CHECK();
+                    cs.launches += 2;
+                }
+                if (mymedk) {
+                    k_take_rank<<<grid1d(mymedk, 256, sms), 256, 0, s>>>(iout, nbig, nmedk, rank, world,
+                                                                         cs.items3m.as<u32>());
+                    GL_LAUNCH_CHECK();
+                    const size_t smem =
+                        (size_t)hpass_ws_words(128, kHPassCount, bloom_words<HCfg<128>::BLOG>()) * sizeof(u32);
+                    smem_attr(k_hpass_block<kHPassCount, 128>, smem, gr.device);
+                    const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + mybig,
+                                     cs.tl_n.as<u32>() + mybig};
+                    k_hpass_block<kHPassCount, 128><<<blocks_m, HCfg<128>::THREADS, smem, s>>>(
+                        g, cs.items3m.as<u32>(), mymedk, counters + 8, cs.t.as<u32>(), d_partials, nullptr, 0,
+                        cs.hlist.as<uint2>(), hcap_m, TL);
+                    GL_LAUNCH_CHECK();
+                    cs.launches += 2;
+                }
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig, nsmall, rank, world,
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmedk, nsmall, rank, world,
                                                                       cs.items3s.as<u32>());
                 GL_LAUNCH_CHECK();
                 k_hpass_warp<kHPassCount><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
@@ -1555,13 +1593,23 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     // triangle sums over the same vertex shares as this rank's H-pass
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40;
     if (g.m && cs.n_items3b) {
-        const unsigned blocks = (unsigned)sms * 2;
-        const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassSums) * sizeof(u32);
-        smem_attr(k_hpass_block<kHPassSums>, smem, gr.device);
+        const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassSums, bloom_words<HCfg<768>::BLOG>()) * sizeof(u32);
+        smem_attr(k_hpass_block<kHPassSums, 768>, smem, gr.device);
         const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
-        k_hpass_block<kHPassSums><<<blocks, kHBlockThreads, smem, s>>>(
+        k_hpass_block<kHPassSums, 768><<<(unsigned)sms * HCfg<768>::MINB, HCfg<768>::THREADS, smem, s>>>(
             g, cs.items3b.as<u32>(), cs.n_items3b, counters + 5, cs.t.as<u32>(), d_partials,
             cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, nullptr, 0, TL);
+        GL_LAUNCH_CHECK();
+        cs.launches += 1;
+    }
+    if (g.m && cs.n_items3m) {
+        const size_t smem = (size_t)hpass_ws_words(128, kHPassSums, bloom_words<HCfg<128>::BLOG>()) * sizeof(u32);
+        smem_attr(k_hpass_block<kHPassSums, 128>, smem, gr.device);
+        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + cs.n_items3b,
+                         cs.tl_n.as<u32>() + cs.n_items3b};
+        k_hpass_block<kHPassSums, 128><<<(unsigned)sms * HCfg<128>::MINB, HCfg<128>::THREADS, smem, s>>>(
+            g, cs.items3m.as<u32>(), cs.n_items3m, counters + 9, cs.t.as<u32>(), d_partials, nullptr, 0, nullptr, 0,
+            TL);
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     }

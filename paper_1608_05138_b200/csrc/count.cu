@@ -671,14 +671,17 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
 // to per-adjacency-slot accumulators (consecutive wedges of a run are
 // consecutive slots), folded into edge rows by k_fold_slots.
 
-__device__ __forceinline__ void w_inc(u32* W, u32 i, bool half) {
-    if (half)
-        atomicAdd(&W[i >> 1], 1u << ((i & 1) << 4));
-    else
-        atomicAdd(&W[i], 1u);
+// Packed window counters: 2^cl counters of (32 >> cl) bits per word.  The
+// width follows the degree tier of the window's c ids (internal ids ascend
+// with degree): W_a[c] <= deg(c), so ids with degree < 4 take 2-bit counters,
+// < 16 4-bit, < 256 8-bit, < 65536 16-bit, the rest 32-bit -- the window over
+// low-degree ids is up to 16x wider than a 32-bit one.
+__device__ __forceinline__ void w_inc(u32* W, u32 i, u32 cl) {
+    atomicAdd(&W[i >> cl], 1u << ((i & ((1u << cl) - 1u)) << (5 - cl)));
 }
-__device__ __forceinline__ u32 w_get(const u32* W, u32 i, bool half) {
-    return half ? (W[i >> 1] >> ((i & 1) << 4)) & 0xffffu : W[i];
+__device__ __forceinline__ u32 w_get(const u32* W, u32 i, u32 cl) {
+    const u32 v = W[i >> cl] >> ((i & ((1u << cl) - 1u)) << (5 - cl));
+    return cl == 0 ? v : v & ((1u << (32u >> cl)) - 1u);
 }
 
 // first index in [lo, hi) with a[idx] >= x, galloping from lo: runs inside a
@@ -749,7 +752,7 @@ template <int KIND> __host__ __device__ constexpr u32 cyc_smem_words() {
 
 
 template <int KIND>
-__device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, bool half) {
+__device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, u32 cl) {
     constexpr u32 NS = 1u << Cyc<KIND>::LOG;
     if (Cyc<KIND>::HASH) {
         u32* keys = W;
@@ -765,41 +768,35 @@ __device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, bool half) {
         }
         atomicAdd(&W[NS + (h >> 1)], 1u << ((h & 1) << 4));
     } else {
-        w_inc(W, c - lo, half);
+        w_inc(W, c - lo, cl);
     }
 }
 template <int KIND>
-__device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, bool half) {
+__device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, u32 cl) {
     constexpr u32 NS = 1u << Cyc<KIND>::LOG;
     if (Cyc<KIND>::HASH) {
         u32 h = (c * 0x9E3779B1u) >> (32 - Cyc<KIND>::LOG);
         while (W[h] != c) h = (h + 1) & (NS - 1);
         return (W[NS + (h >> 1)] >> ((h & 1) << 4)) & 0xffffu;
     } else {
-        return w_get(W, c - lo, half);
+        return w_get(W, c - lo, cl);
     }
 }
 // dense windows only: the hash is always bulk-cleared (a deleted key would
 // break the probe chains of the clears still to come)
-__device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, bool half) {
-    const u32 ci = c - lo;
-    if (half)
-        W[ci >> 1] = 0;
-    else
-        W[ci] = 0;
-}
+__device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, u32 cl) { W[(c - lo) >> cl] = 0; }
 
 template <int KIND, int PASS>
-__device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, bool half, i64* __restrict__ slot_acc, u64 slot,
+__device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, u32 cl, i64* __restrict__ slot_acc, u64 slot,
                                          u64& val) {
     if (PASS == 0) {
-        tab_inc<KIND>(W, cv, lo, half);
+        tab_inc<KIND>(W, cv, lo, cl);
     } else if (PASS == 1) {
-        const u32 v = tab_get<KIND>(W, cv, lo, half) - 1u;
+        const u32 v = tab_get<KIND>(W, cv, lo, cl) - 1u;
         if (v) atomic_add_i64(&slot_acc[slot], (i64)v);
         val = v;
     } else {
-        tab_clear_one(W, cv, lo, half);
+        tab_clear_one(W, cv, lo, cl);
     }
 }
 
@@ -835,7 +832,7 @@ constexpr int kUnroll = 8; // uniform-path rounds with loads in flight per lane
 
 template <int KIND, int PASS>
 __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,
-                                            u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
+                                            u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
     const u32 lane = lane_id();
     if (kb >= ke) return;
     u32 bs = warp_upper_bound(S.pre, nnz + 1, kb);
@@ -857,7 +854,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                 for (int u = 0; u < kUnroll; ++u) {
                     if (cv[u] != kEmpty) {
                         u64 v = 0;
-                        wedge_op<KIND, PASS>(W, cv[u], lo, half, slot_acc, sbase + 32u * (r + u), v);
+                        wedge_op<KIND, PASS>(W, cv[u], lo, cl, slot_acc, sbase + 32u * (r + u), v);
                         acc += v;
                     }
                 }
@@ -885,7 +882,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             u64 v = 0;
             if (valid) {
                 const u64 slot = (u64)S.rs[q] + (k - opi);
-                wedge_op<KIND, PASS>(W, __ldg(g.adj + slot), lo, half, slot_acc, slot, v);
+                wedge_op<KIND, PASS>(W, __ldg(g.adj + slot), lo, cl, slot_acc, slot, v);
             }
             if (PASS == 1) {
                 const u32 off = k - opi;
@@ -929,7 +926,7 @@ __device__ __forceinline__ u32 grab_size(u32 remaining, u32 nwarps) {
 // consecutive slots), folded into edge rows by k_fold_slots.
 template <int KIND, int PASS>
 __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u32 nnz, u32 T, u32* counter, u32* W,
-                                          u32 lo, bool half, u64 abase, i64* __restrict__ slot_acc) {
+                                          u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
     const u32 nwarps = blockDim.x >> 5;
     for (;;) {
         u32 k0 = 0, grab = 0;
@@ -941,7 +938,7 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
         k0 = __shfl_sync(0xffffffffu, k0, 0);
         grab = __shfl_sync(0xffffffffu, grab, 0);
         if (k0 >= T) break;
-        window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, half, abase, slot_acc);
+        window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, cl, abase, slot_acc);
     }
 }
 
@@ -952,7 +949,7 @@ __device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..2
 template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-              i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap) {
+              i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap, uint4 tiers) {
     constexpr bool HASH = Cyc<KIND>::HASH;
     constexpr int THREADS = Cyc<KIND>::THREADS;
     constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
@@ -996,10 +993,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u64 E0 = g.loff[a];
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
-        const bool half = HASH || nb < 65536u;
-        u32 span = half ? 2u * kWindow : (u32)kWindow;
-        // keep nb * span < 2^31: window wedge counts and indices are u32
-        if ((u64)nb * span >= (1ull << 31)) span = (u32)((1ull << 31) / nb) & ~1u;
+
         if (threadIdx.x == 0) s_next = HASH ? 0u : kEmpty;
         __syncthreads();
         // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at 0
@@ -1021,8 +1015,18 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         u32* cur = S.cur;
         u32* nxt = S.hpos;
         u32 win = 0;
-        for (u32 lo = s_next; lo < a; lo = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a), ++win) {
-            const u32 hi = HASH ? a : ((u64)lo + span < (u64)a ? lo + span : a);
+        (void)win;
+        for (u32 lo = s_next, hi = 0; lo < a; lo = hi, ++win) {
+            // window [lo, hi): inside one degree tier, counters of that tier's width
+            u32 cl = 1, tend = a;
+            if (!HASH) {
+                cl = lo < tiers.x ? 4u : lo < tiers.y ? 3u : lo < tiers.z ? 2u : lo < tiers.w ? 1u : 0u;
+                tend = lo < tiers.x ? tiers.x : lo < tiers.y ? tiers.y : lo < tiers.z ? tiers.z : lo < tiers.w ? tiers.w : a;
+            }
+            u64 span = (u64)kWindow << cl;
+            // keep nb * span < 2^31: window wedge counts and indices are u32
+            if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
+            hi = HASH ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)a);
 
             // run ends; runs are ordered thread-major (thread t owns b = t + i*THREADS,
             // coalesced), so one block scan of per-thread (runs, wedges) places them
@@ -1071,28 +1075,28 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 const bool bulk_clear = HASH || T > kWords / 8;
                 {
                     if (nnz <= kMeta) // shared-memory metadata: LDS in the walk
-                        grab_pass<KIND, 0>(g, Msm, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 0>(g, Msm, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
                     else
-                        grab_pass<KIND, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
                 }
                 __syncthreads();
                 GL_PROF_MARK(3);
                 {
                     if (nnz <= kMeta)
-                        grab_pass<KIND, 1>(g, Msm, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 1>(g, Msm, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
                     else
-                        grab_pass<KIND, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
                 }
                 __syncthreads();
                 GL_PROF_MARK(4);
                 if (bulk_clear) {
-                    const u32 words = HASH ? kWords : (half ? (hi - lo + 1) >> 1 : hi - lo);
+                    const u32 words = HASH ? kWords : (hi - lo + (1u << cl) - 1u) >> cl;
                     for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
                 } else if (!HASH) {
                     if (nnz <= kMeta)
-                        grab_pass<KIND, 2>(g, Msm, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 2>(g, Msm, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
                     else
-                        grab_pass<KIND, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, half, abase, slot_acc);
+                        grab_pass<KIND, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
                 }
             }
             GL_PROF_SYNC_MARK(7);
@@ -1295,6 +1299,25 @@ __global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u32* __rest
     if (lm) atomicAdd(n_mid, lm);
     if (lq) atomicAdd(n_smid, lq);
     if (ls) atomicAdd(n_small, ls);
+}
+
+// degree tiers of the window counters: #vertices with degree < 4, 16, 256,
+// 65536 = the first internal id of the next tier (ids ascend with degree)
+__global__ void k_tiers(DevGraph g, unsigned* __restrict__ out) {
+    unsigned c[4] = {0, 0, 0, 0};
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < g.n; v += (u64)gridDim.x * blockDim.x) {
+        const u32 d = g.deg[v];
+        c[0] += d < 4u;
+        c[1] += d < 16u;
+        c[2] += d < 256u;
+        c[3] += d < 65536u;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        unsigned v = c[i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&out[i], v);
+    }
 }
 
 // rank's share of a cost-sorted list: sorted positions p with p % world == rank
@@ -1513,6 +1536,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* iout = iin + (n + 1);
             k_top_keys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,
                                                            counters + 16, counters + 11);
+            k_tiers<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 22));
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
@@ -1520,6 +1544,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             GL_CUDA(cudaMemcpyAsync(cc, counters, sizeof(cc), cudaMemcpyDeviceToHost, s));
             const u64 wtot = read_dev(cs.wpre.as<u64>() + m, s);
             const u64 nbig = cc[10], nmid = cc[15], nsmid = cc[16], nsmall = cc[11];
+            const uint4 tiers = make_uint4((u32)cc[22], (u32)(cc[22] >> 32), (u32)cc[23], (u32)(cc[23] >> 32));
             cs.work[2] = 12 * wtot / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
             const u64 mybig = rank_share(nbig, rank, world);
@@ -1549,7 +1574,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
                     smem_attr(k_cycle_block<K>, smem, gr.device);
                     k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s>>>(
-                        g, list, count, queue, cs.slots.as<i64>(), scratch, cap);
+                        g, list, count, queue, cs.slots.as<i64>(), scratch, cap, tiers);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };

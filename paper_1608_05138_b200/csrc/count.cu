@@ -846,18 +846,27 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             const u32 nfull = (stop - k0) >> 5;
             const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
             u64 acc = 0;
-            for (u32 r = 0; r < nfull; r += kUnroll) {
-                u32 cv[kUnroll];
+            // software pipeline: the next kHalf rounds' loads are in flight
+            // while the current kHalf rounds update the window
+            constexpr int kHalf = kUnroll / 2;
+            u32 cv[kHalf];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) cv[u] = r + u < nfull ? __ldg(g.adj + sbase + 32u * (r + u)) : kEmpty;
+            for (int u = 0; u < kHalf; ++u) cv[u] = (u32)u < nfull ? __ldg(g.adj + sbase + 32u * u) : kEmpty;
+            for (u32 r = 0; r < nfull; r += kHalf) {
+                u32 nx[kHalf];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < kHalf; ++u)
+                    nx[u] = r + kHalf + u < nfull ? __ldg(g.adj + sbase + 32u * (r + kHalf + u)) : kEmpty;
+#pragma unroll
+                for (int u = 0; u < kHalf; ++u) {
                     if (cv[u] != kEmpty) {
                         u64 v = 0;
                         wedge_op<KIND, PASS>(W, cv[u], lo, cl, slot_acc, sbase + 32u * (r + u), v);
                         acc += v;
                     }
                 }
+#pragma unroll
+                for (int u = 0; u < kHalf; ++u) cv[u] = nx[u];
             }
             if (PASS == 1) {
                 acc = warp_sum_u64(acc);
@@ -865,35 +874,45 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             }
             k0 += nfull << 5;
         } else {
-            // mixed round [k0, k0 + 32)
+            // mixed round [k0, k0 + 32): runs bs, bs+1, ... start at pre[bs+j];
+            // one OR-reduction gives the bitmask of run starts inside the round,
+            // from which every lane reads its run (popcount), its offset and
+            // its segment (highest start at or below it)
             const u32 k = k0 + lane;
             const bool valid = k < ke;
             const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
-            u32 owner = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const u32 cand = owner + step;
-                const u32 ex = __shfl_sync(0xffffffffu, pi, cand & 31);
-                if (cand < 32 && ex <= k) owner = cand;
-            }
-            const u32 opi = __shfl_sync(0xffffffffu, pi, owner);
-            const u32 onx = __shfl_sync(0xffffffffu, pi, (owner + 1) & 31);
+            const u32 rel = pi - k0; // >= 1 for lanes >= 1 (pre strictly increasing)
+            const u32 starts = __reduce_or_sync(0xffffffffu, (lane > 0 && rel < 32u) ? 1u << rel : 0u);
+            const u32 le = starts & (0xffffffffu >> (31 - lane)); // starts at or below this lane
+            const u32 owner = __popc(le);
             const u32 q = bs + owner;
+            const u32 seg0 = owner ? 31u - __clz(le) : 0u;
+            const u32 pi0 = __shfl_sync(0xffffffffu, pi, 0); // all lanes: full-mask shuffle
+            const u32 off = owner ? lane - seg0 : k - pi0;
             u64 v = 0;
             if (valid) {
-                const u64 slot = (u64)S.rs[q] + (k - opi);
+                const u64 slot = (u64)S.rs[q] + off;
                 wedge_op<KIND, PASS>(W, __ldg(g.adj + slot), lo, cl, slot_acc, slot, v);
             }
             if (PASS == 1) {
-                const u32 off = k - opi;
-                const u32 seg0 = lane > off ? lane - off : 0u;
+                const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));
+                if (cl) {
+                    // counters of <= 16 bits: the segment sum fits u32
+                    u32 v32 = (u32)v;
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const u64 t = __shfl_up_sync(0xffffffffu, v, d);
-                    if (lane >= seg0 + (u32)d) v += t;
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const u32 t = __shfl_up_sync(0xffffffffu, v32, d);
+                        if (lane >= seg0 + (u32)d) v32 += t;
+                    }
+                    if (tail && v32) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v32);
+                } else {
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const u64 t = __shfl_up_sync(0xffffffffu, v, d);
+                        if (lane >= seg0 + (u32)d) v += t;
+                    }
+                    if (tail && v) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v);
                 }
-                const bool tail = valid && (lane == 31 || k + 1 == ke || (owner < 31 && k + 1 == onx));
-                if (tail && v) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v);
             }
             k0 += 32;
             bs = __shfl_sync(0xffffffffu, q, 31);

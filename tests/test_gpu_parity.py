@@ -271,3 +271,31 @@ def test_rmat20_properties_and_sample(cuda_device):
     assert np.array_equal(ref[:, 0], t[ids].astype(np.uint64))
     assert np.array_equal(ref[:, 3], x7[ids])
     assert np.array_equal(ref[:, 4], x10[ids])
+
+
+def test_cli_count_spec_examples(tmp_path):
+    """SPEC cli cmd_count examples through the C++ driver: K4 -> "X7":"1";
+    --micro on C4 -> 4 rows with x10 = 1; every golden graph's X matches."""
+    import json
+    import subprocess
+    tool = os.path.join(os.path.dirname(gl.lib_path()), "graphlet_count")
+    k4 = tmp_path / "k4.txt"
+    k4.write_text("".join(f"{a} {b}\n" for a in range(4) for b in range(a + 1, 4)))
+    doc = json.loads(subprocess.run([tool, "count", str(k4)], capture_output=True, text=True, check=True).stdout)
+    assert doc["counts"]["X7"] == "1" and doc["n"] == 4 and doc["m"] == 6
+    c4 = tmp_path / "c4.txt"
+    c4.write_text("0 1\n1 2\n2 3\n3 0\n")
+    micro = tmp_path / "micro.csv"
+    subprocess.run([tool, "count", str(c4), "--micro", str(micro)], check=True, capture_output=True)
+    rows = micro.read_text().strip().splitlines()
+    assert rows[0].startswith("edge_id,") and len(rows) == 5
+    assert all(r.split(",")[5] == "1" for r in rows[1:])
+    for name in golden_cases():
+        d = load_golden(name)
+        f = tmp_path / f"{name}.txt"
+        f.write_text("".join(f"{a} {b}\n" for a, b in d["pairs"]))
+        if not d["pairs"]:
+            continue
+        doc = json.loads(subprocess.run([tool, "count", str(f)], capture_output=True, text=True,
+                                        check=True).stdout)
+        assert [doc["counts"][f"X{i}"] for i in range(1, 18)] == d["X"][1:], name

@@ -136,3 +136,25 @@ def test_device_calls_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(gl.CudaError):
         gl.Graph.build([(1, 2), (2, 3)])
+
+
+def test_cpp_api_mirror_host_calls(tmp_path):
+    """include/graphlet_b200.hpp (C++ mirror of the reference API) compiles
+    against the product library; its host-only calls behave like the reference."""
+    exe = tmp_path / "cpp_api_check"
+    libdir = os.path.dirname(gl.lib_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp_api_check.cpp"), "-o", str(exe), "-L", libdir,
+                    "-lgraphlet_b200", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "ok"
+
+
+def test_cli_usage_and_errors(tmp_path):
+    tool = os.path.join(os.path.dirname(gl.lib_path()), "graphlet_count")
+    assert subprocess.run([tool], capture_output=True).returncode == 2
+    assert subprocess.run([tool, "count", str(tmp_path / "missing.txt")], capture_output=True).returncode == 1
+    bad = tmp_path / "bad.txt"
+    bad.write_text("1 2\n3 x\n")
+    r = subprocess.run([tool, "count", str(bad)], capture_output=True, text=True)
+    assert r.returncode == 2 and "line 2" in r.stderr

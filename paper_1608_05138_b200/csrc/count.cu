@@ -394,7 +394,20 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         const u32 bb = bloom_bit<BLOG>(x);
         atomicOr(&bloom[bb >> 5], 1u << (bb & 31));
     }
+    if (MODE == kHPassCount && threadIdx.x == 0) {
+        // reserve C(k,2) records of the device-wide list up front, so phase 1
+        // appends the H-edges straight into it (no per-block copy)
+        u64 b = kNoList;
+        if (TL.rec) {
+            const u64 need = (u64)k * (k - 1) / 2;
+            b = atomicAdd(TL.count, (unsigned long long)need);
+            if (b + need > TL.cap) b = kNoList;
+            TL.base[idx] = b;
+        }
+        s_base = b;
+    }
     __syncthreads();
+    uint2* const hout = (MODE == kHPassCount && s_base != kNoList) ? TL.rec + s_base : hlist;
     const u32 xmax = xs[k - 1];
     // phase 1: warps grab members i < k-1 and stream U(x_i)
     for (;;) {
@@ -479,7 +492,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
                         u32 base = 0;
                         if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
                         base = __shfl_sync(0xffffffffu, base, 0);
-                        if (hit) hlist[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
+                        if (hit) hout[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
                     }
                 } else if (hit) {
                     const u64 txy = t[e];
@@ -498,22 +511,11 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     }
     __syncthreads();
     if (MODE == kHPassCount) {
-        // phase 2: stream the H-edges (and keep them for the sums pass)
+        // phase 2: stream the H-edges (kept in the device-wide list when it had room)
         const u32 nh = s_nh;
-        if (TL.rec) {
-            if (threadIdx.x == 0) {
-                u64 b = atomicAdd(TL.count, (unsigned long long)nh);
-                if (b + nh > TL.cap) b = kNoList;
-                TL.base[idx] = b;
-                TL.n[idx] = nh;
-                s_base = b;
-            }
-            __syncthreads();
-        }
-        const u64 tb = TL.rec ? s_base : kNoList;
+        if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
         for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
-            const uint2 he = hlist[h];
-            if (tb != kNoList) TL.rec[tb + h] = he;
+            const uint2 he = hout[h];
             const u32 i = he.x & 0xffffu, j = he.x >> 16;
             const u32* ri = rows + (u64)i * RS;
             const u32* rj = rows + (u64)j * RS;
@@ -1273,8 +1275,7 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
                 cls = k > 128 ? 3 : 2;
                 if (cls == 3) ++ll; else ++lm;
                 mx = q > mx ? q : mx;
-                const u64 pairs = k * (k - 1) / 2;
-                hb += pairs < q ? pairs : q;
+                hb += k * (k - 1) / 2; // the counting pass reserves C(k,2) records per vertex
             } else {
                 ++ls;
             }

@@ -252,6 +252,20 @@ def test_device_generated_graph_matches_host(cuda_device):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("scale", [16, 17])
+def test_rmat_full_parity_larger(cuda_device, scale):
+    """Every micro record and X_1..X_17 vs the oracle's per-edge hash pipeline
+    (the reference algorithm) at RMAT 16/17: hub tops, every cycle-kernel kind,
+    several degree-tier windows, both block H-pass classes."""
+    pairs = gl.generate_rmat(scale, 16, seed=100 + scale)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
+@pytest.mark.slow
 def test_rmat20_properties_and_sample(cuda_device):
     """BASELINE configs[1] at full size: size-independent properties plus a
     sampled per-edge comparison with the oracle's hash pipeline."""

@@ -48,8 +48,12 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--graph", choices=["rmat", "ba"], default="rmat",
+                    help="rmat: configs[1]/[3]/[4] (RMAT/Kronecker scale S); ba: configs[2] (Barabasi-Albert)")
     ap.add_argument("--scale", type=int, default=20)
     ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--ba-n", type=int, default=4_000_000)
+    ap.add_argument("--ba-attach", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -66,9 +70,19 @@ def dist_env():
 
 
 def workload(args):
+    if args.graph == "ba":
+        return {"workload": f"Barabasi-Albert n={args.ba_n} attach={args.ba_attach} (seed {args.seed}), "
+                            "k=4 macro+micro", "ba_n": args.ba_n, "ba_attach": args.ba_attach}
     return {"workload": f"RMAT scale-{args.scale} (2^{args.scale} vertex labels, edge factor {args.edge_factor}, "
                         f"a,b,c=.57,.19,.19, seed {args.seed}), k=4 macro+micro",
             "scale": args.scale, "edge_factor": args.edge_factor}
+
+
+def host_pairs(args):
+    import paper_1608_05138_b200 as gl
+    if args.graph == "ba":
+        return gl.generate_ba(args.ba_n, args.ba_attach, seed=args.seed)
+    return gl.generate_rmat(args.scale, args.edge_factor, seed=args.seed)
 
 
 # --------------------------------------------------------------------- clocks
@@ -162,8 +176,7 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
-    import paper_1608_05138_b200 as gl
-    pairs = gl.generate_rmat(args.scale, args.edge_factor, seed=args.seed)
+    pairs = host_pairs(args)
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     rates, cores, kind, desc = cpu_sample_run(pairs, per_step, steps=args.steps + args.warmup)
     rates = rates[args.warmup:] or rates
@@ -198,10 +211,16 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    # ---- input generated in HBM, CSR built on device (untimed setup)
-    count = args.edge_factor << args.scale
-    d_pairs = torch.empty(2 * count, dtype=torch.int64, device=dev)
-    gl.generate_rmat_device(args.scale, args.edge_factor, d_pairs.data_ptr(), local, seed=args.seed)
+    # ---- input generated in HBM (RMAT) or on the host (BA), CSR built on device (untimed setup)
+    hp = None
+    if args.graph == "ba":
+        hp = host_pairs(args)
+        count = len(hp)
+        d_pairs = torch.from_numpy(hp.view(np.int64).reshape(-1)).to(dev)
+    else:
+        count = args.edge_factor << args.scale
+        d_pairs = torch.empty(2 * count, dtype=torch.int64, device=dev)
+        gl.generate_rmat_device(args.scale, args.edge_factor, d_pairs.data_ptr(), local, seed=args.seed)
     torch.cuda.synchronize()
     tb = time.perf_counter()
     g = gl.Graph.build_device(d_pairs.data_ptr(), count, local)
@@ -275,8 +294,8 @@ def run_ours(args):
     # ---- e2e through the public C-ABI from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host_pairs = gl.generate_rmat(args.scale, args.edge_factor, seed=args.seed)
-        pin_in = torch.from_numpy(host_pairs.view(np.int64).reshape(-1)).pin_memory()
+        hpairs = hp if hp is not None else host_pairs(args)
+        pin_in = torch.from_numpy(hpairs.view(np.int64).reshape(-1)).pin_memory()
         shard_n = e - b
         pin_t = torch.empty(max(1, shard_n), dtype=torch.int32).pin_memory()
         pin_x7 = torch.empty(max(1, shard_n), dtype=torch.int64).pin_memory()
@@ -311,8 +330,8 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        host_pairs = gl.generate_rmat(args.scale, args.edge_factor, seed=args.seed)
-        rates, cores, kind, desc = cpu_sample_run(host_pairs, args.cpu_seconds)
+        hpairs = hp if hp is not None else host_pairs(args)
+        rates, cores, kind, desc = cpu_sample_run(hpairs, args.cpu_seconds)
         cpu = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}
 
     if rank == 0:
@@ -320,7 +339,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic (RMAT generated on device, seed 1)",
+            "data": ("synthetic (BA generated on the host, seed %d)" % args.seed if args.graph == "ba"
+                     else "synthetic (RMAT generated on device, seed %d)" % args.seed),
             "config": dict(workload(args), n=n, m=m, parallelism=f"replicated graph, {world} rank work shares",
                            l2="flushed (256 MiB write) before every step, outside the timed events"),
             "e2e": e2e,

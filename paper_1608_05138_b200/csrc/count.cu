@@ -700,10 +700,12 @@ __device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64
     }
 }
 
+constexpr int kNcBatch = 8; // b's whose window test loads are issued together
+
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
-    u32 *cur, *hpos, *rend, *pre, *rj, *rs;
-    u64 *rb, *pre64;
+    u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin;
+    u64* rb;
 };
 // compacted runs of one window: wedge prefix pre[nnz+1], first adjacency slot
 // rs[q] (u32: 2m < 2^32 is checked on the host), lower-neighbour index rj[q];
@@ -720,7 +722,8 @@ __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     s.rj = base + 4 * (u64)cap + 1;
     s.rs = base + 5 * (u64)cap + 1;
     s.rb = reinterpret_cast<u64*>(base + ((6 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
-    s.pre64 = s.rb + cap;
+    s.nextc = reinterpret_cast<u32*>(s.rb + cap); // c at the cursor (kEmpty: row done)
+    s.rwin = s.nextc + cap;                        // window of b's last recorded run
     return s;
 }
 __host__ __device__ inline u64 big_scratch_words(u32 cap) { return 10ull * cap + 8; }
@@ -1025,18 +1028,18 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             S.rb[j] = rb;
             S.rend[j] = re;
             S.cur[j] = 0;
-            if (!HASH && re > 0) atomicMin(&s_next, g.adj[rb]);
+            const u32 c = re > 0 ? g.adj[rb] : kEmpty;
+            S.nextc[j] = c;
+            S.rwin[j] = kEmpty;
+            if (!HASH && c != kEmpty) atomicMin(&s_next, c);
         }
         __syncthreads();
         GL_PROF_MARK(0);
         GL_PROF_ADD(10, 1);
-        // windows [lo, lo+span) from the smallest c on, fixed stride: the run
-        // of b in a window is [cur_b, nxt_b) and the window's ends become the
-        // next window's cursors (pointer swap, no extra pass)
-        u32* cur = S.cur;
-        u32* nxt = S.hpos;
+        // Windows from the smallest c on.  Each b keeps its cursor and the c
+        // value under it (nextc), so a window only gallops the b's whose next c
+        // falls inside it; for the others one coalesced nextc load suffices.
         u32 win = 0;
-        (void)win;
         for (u32 lo = s_next, hi = 0; lo < a; lo = hi, ++win) {
             // window [lo, hi): inside one degree tier, counters of that tier's width
             u32 cl = 1, tend = a;
@@ -1049,15 +1052,28 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
             hi = HASH ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)a);
 
-            // run ends; runs are ordered thread-major (thread t owns b = t + i*THREADS,
-            // coalesced), so one block scan of per-thread (runs, wedges) places them
+            // run ends of the b's with a c in [lo, hi); runs are ordered
+            // thread-major (thread t owns b = t + i*THREADS), so one block scan
+            // of per-thread (runs, wedges) places them
             u32 my_runs = 0, my_wedges = 0;
-            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
-                const u32 c0 = cur[j];
-                const u64 rb = S.rb[j];
-                const u32 h = HASH ? S.rend[j] : (u32)(gallop_lower_bound(g.adj, rb + c0, rb + S.rend[j], hi) - rb);
-                nxt[j] = h;
-                if (h > c0) {
+            for (u32 j0 = threadIdx.x; j0 < nb; j0 += kNcBatch * THREADS) {
+                u32 nc[kNcBatch];
+#pragma unroll
+                for (int u = 0; u < kNcBatch; ++u) {
+                    const u32 j = j0 + u * THREADS;
+                    nc[u] = j < nb ? S.nextc[j] : kEmpty;
+                }
+#pragma unroll
+                for (int u = 0; u < kNcBatch; ++u) {
+                    if (nc[u] >= hi) continue; // no c of b in this window (kEmpty >= hi)
+                    const u32 j = j0 + u * THREADS;
+                    const u32 c0 = S.cur[j], re = S.rend[j];
+                    const u64 rb = S.rb[j];
+                    const u32 h = HASH ? re : (u32)(gallop_lower_bound(g.adj, rb + c0, rb + re, hi) - rb);
+                    S.hpos[j] = c0; // run start
+                    S.rwin[j] = win;
+                    S.cur[j] = h;
+                    S.nextc[j] = h < re ? g.adj[rb + h] : kEmpty;
                     ++my_runs;
                     my_wedges += h - c0;
                 }
@@ -1077,9 +1093,18 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             const RunMeta M = nnz <= kMeta ? Msm : Mgl;
             if (my_runs) {
                 u32 q = (u32)(mine >> 32), w = (u32)mine;
-                for (u32 j = threadIdx.x; j < nb; j += THREADS) {
-                    const u32 c0 = cur[j], h = nxt[j];
-                    if (h > c0) {
+                for (u32 j0 = threadIdx.x; j0 < nb && q < (u32)(mine >> 32) + my_runs; j0 += kNcBatch * THREADS) {
+                    u32 rw[kNcBatch];
+#pragma unroll
+                    for (int u = 0; u < kNcBatch; ++u) {
+                        const u32 j = j0 + u * THREADS;
+                        rw[u] = j < nb ? S.rwin[j] : kEmpty;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kNcBatch; ++u) {
+                        if (rw[u] != win) continue;
+                        const u32 j = j0 + u * THREADS;
+                        const u32 c0 = S.hpos[j], h = S.cur[j];
                         M.rj[q] = j;
                         M.rs[q] = (u32)(S.rb[j] + c0);
                         M.pre[q] = w;
@@ -1121,9 +1146,6 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 }
             }
             GL_PROF_SYNC_MARK(7);
-            u32* tmp = cur;
-            cur = nxt;
-            nxt = tmp;
             __syncthreads();
             GL_PROF_MARK(5);
         }

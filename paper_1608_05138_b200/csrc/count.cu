@@ -147,6 +147,12 @@ __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
+// 2 <= k <= 32: one warp per vertex a.  Phase 1 streams every member's upper
+// list U(x_i) with the whole warp (coalesced) and looks each entry up in
+// U(a) (32 sorted ids in shared memory, 5-step search); a hit sets bit j of
+// row i and records the edge id of (x_i, x_j) in a 32 x 32 shared table, so
+// phase 2 needs no global search.  kHPassCount: t and x7 credits as in the
+// block kernel; kHPassSums: the three S credits of every triangle.
 template <int MODE>
 __global__ void __launch_bounds__(kHWarpsPerBlock * 32)
 k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
@@ -154,7 +160,10 @@ k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lo
     __shared__ u32 s_x[kHWarpsPerBlock][32];
     __shared__ u32 s_row[kHWarpsPerBlock][32];
     __shared__ u32 s_ta[kHWarpsPerBlock][32];
+    __shared__ u32 s_e[kHWarpsPerBlock][32][33]; // edge id of (x_i, x_j), j > i (padded)
     __shared__ unsigned long long s_acc[kHWarpsPerBlock][32];
+    __shared__ u32 s_pre[kHWarpsPerBlock][32], s_ppre[kHWarpsPerBlock][32];
+    __shared__ u64 s_xb[kHWarpsPerBlock][32], s_xe[kHWarpsPerBlock][32];
     const u32 lane = lane_id(), wib = threadIdx.x >> 5;
     u32* xs = s_x[wib];
     u32* rows = s_row[wib];
@@ -168,43 +177,106 @@ k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lo
         const u32 a = items[idx];
         const u64 ub = u_begin(g, a);
         const u32 k = (u32)(g.off[a + 1] - ub);
-        u32 x = 0;
         u64 xb = 0, xe = 0;
         if (lane < k) {
-            x = g.adj[ub + lane];
+            const u32 x = g.adj[ub + lane];
+            xs[lane] = x;
             xb = u_begin(g, x);
             xe = g.off[x + 1];
             if (MODE == kHPassSums) ta[lane] = t[g.eid[ub + lane]];
+        } else {
+            xs[lane] = kEmpty; // sorts after every id: searches stay inside [0, k)
         }
-        xs[lane] = x;
+        rows[lane] = 0;
         acc[lane] = 0;
         __syncwarp();
-        // phase 1: upper row, bit j > lane set iff x_j in U(x)
-        u32 row = 0;
-        if (lane + 1 < k) {
-            const u32 rem = k - 1 - lane;
-            if (xe - xb <= rem) {
-                for (u64 p = xb; p < xe; ++p) {
-                    u32 y = g.adj[p];
-                    u32 j = lower_bound_dev<u32, u32>(xs, lane + 1, k, y);
-                    if (j < k && xs[j] == y) row |= 1u << j;
+        const u32 xmax = xs[k - 1];
+        // phase 1: member i's H-row by streaming U(x_i) when it is short
+        // (|U(x_i)| <= 8 * rem_i, rem_i = k-1-i) or else by probing the rem_i
+        // candidates x_j (j > i) into U(x_i) with binary searches.  Both work
+        // lists are flattened over the warp (prefix sums in shared memory, a
+        // 5-step search maps a lane to its member), 4 rounds in flight.
+        const u32 rem = lane + 1 < k ? k - 1 - lane : 0u;
+        const u32 ul = (u32)(xe - xb);
+        const bool probe = rem && ul > 8u * rem;
+        const u32 slen = rem && !probe ? ul : 0u, plen = probe ? rem : 0u;
+        u32 sin = slen, pin = plen;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 o1 = __shfl_up_sync(0xffffffffu, sin, d);
+            const u32 o2 = __shfl_up_sync(0xffffffffu, pin, d);
+            if (lane >= (u32)d) {
+                sin += o1;
+                pin += o2;
+            }
+        }
+        const u32 stot = __shfl_sync(0xffffffffu, sin, 31), ptot = __shfl_sync(0xffffffffu, pin, 31);
+        s_pre[wib][lane] = sin - slen;
+        s_ppre[wib][lane] = pin - plen;
+        s_xb[wib][lane] = xb;
+        s_xe[wib][lane] = xe;
+        __syncwarp();
+        for (u32 r0 = 0; r0 < stot; r0 += 128) {
+            u32 yv[4], iv[4];
+            u64 pv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 r = r0 + 32u * u + lane;
+                iv[u] = 0;
+                yv[u] = kEmpty;
+                if (r < stot) {
+                    u32 mi = 0; // last member whose prefix <= r (empty lists share prefixes)
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (mi + step < 32 && s_pre[wib][mi + step] <= r) mi += step;
+                    iv[u] = mi;
+                    pv[u] = s_xb[wib][mi] + (r - s_pre[wib][mi]);
+                    yv[u] = g.adj[pv[u]];
                 }
-            } else {
-                for (u32 j = lane + 1; j < k; ++j) {
-                    u32 y = xs[j];
-                    u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
-                    if (p < xe && g.adj[p] == y) row |= 1u << j;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 y = yv[u];
+                if (y <= xmax) {
+                    u32 lo = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (xs[lo + step - 1] < y) lo += step;
+                    if (xs[lo] == y) { // lo > i: y is above x_i
+                        atomicOr(&rows[iv[u]], 1u << lo);
+                        s_e[wib][iv[u]][lo] = g.eid[pv[u]];
+                    }
                 }
             }
         }
-        // symmetrise: lane j collects the lanes whose upper row names j
+        for (u32 r0 = 0; r0 < ptot; r0 += 32) {
+            const u32 r = r0 + lane;
+            if (r < ptot) {
+                u32 mi = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1)
+                    if (mi + step < 32 && s_ppre[wib][mi + step] <= r) mi += step;
+                const u32 j = mi + 1 + (r - s_ppre[wib][mi]);
+                const u32 y = xs[j];
+                const u64 b1 = s_xe[wib][mi];
+                const u64 pp = lower_bound_dev<u32, u64>(g.adj, s_xb[wib][mi], b1, y);
+                if (pp < b1 && g.adj[pp] == y) {
+                    atomicOr(&rows[mi], 1u << j);
+                    s_e[wib][mi][j] = g.eid[pp];
+                }
+            }
+        }
+        __syncwarp();
+        // symmetrise: lane j collects the members whose upper row names j
+        const u32 row = rows[lane];
         u32 col = 0;
 #pragma unroll 8
         for (int j = 0; j < 32; ++j) {
-            u32 b = __ballot_sync(0xffffffffu, (row >> j) & 1u);
-            if (lane == (u32)j) col = b;
+            const u32 bb = __ballot_sync(0xffffffffu, (row >> j) & 1u);
+            if (lane == (u32)j) col = bb;
         }
         const u32 full = row | col;
+        __syncwarp();
         rows[lane] = full;
         __syncwarp();
         // phase 2: per H-edge (lane, j > lane)
@@ -217,14 +289,12 @@ k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lo
                 const u32 c = __popc(full & rows[j]);
                 tri += c;
                 if ((u32)j > lane) {
-                    const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
-                    const u32 e = g.eid[p];
+                    const u32 e = s_e[wib][lane][j];
                     atomicAdd(&t[e], 1u);
                     if (c) atomic_add_i64(&part[2 * (u64)e], (i64)c);
                 }
             } else {
-                const u64 p = lower_bound_dev<u32, u64>(g.adj, xb, xe, xs[j]);
-                const u32 e = g.eid[p];
+                const u32 e = s_e[wib][lane][j];
                 const u64 txy = t[e];
                 atomic_add_i64(&part[2 * (u64)e + 1], -(i64)((u64)ta[lane] + ta[j]));
                 atomicAdd(&acc[lane], (unsigned long long)(ta[j] + txy));

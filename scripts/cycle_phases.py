@@ -8,8 +8,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("GRAPHLET_B200_LIB", "libgraphlet_b200_prof.so")
 import paper_1608_05138_b200 as gl  # noqa: E402
 
-scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-g = gl.Graph.build(gl.generate_rmat(scale, 16, seed=1))
+arg = sys.argv[1] if len(sys.argv) > 1 else "20"
+if arg == "ba":  # configs[2]: Barabasi-Albert 4M vertices / 64M edges
+    g = gl.Graph.build(gl.generate_ba(4_000_000, 16, seed=1))
+else:
+    g = gl.Graph.build(gl.generate_rmat(int(arg), 16, seed=1))
 def run():
     try:
         g.count()

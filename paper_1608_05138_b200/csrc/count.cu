@@ -147,6 +147,19 @@ __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
+// Persistent H-edge records of the block H-pass: the counting pass appends
+// every H-edge (i | j << 16, e_xy) of vertex a to one device-wide list and
+// records (base, count) per work item; the triangle-sum pass then streams the
+// records instead of re-deriving them (base = kNoList: list full, re-derive).
+struct TriList {
+    uint2* rec;
+    u64 cap;
+    unsigned long long* count;
+    u64* base;   // per work item
+    u32* n;      // per work item
+};
+constexpr u64 kNoList = ~0ull;
+
 // 2 <= k <= 32: one warp per vertex a.  Phase 1 streams every member's upper
 // list U(x_i) with the whole warp (coalesced) and looks each entry up in
 // U(a) (32 sorted ids in shared memory, 5-step search); a hit sets bit j of
@@ -156,7 +169,7 @@ __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
 template <int MODE>
 __global__ void __launch_bounds__(kHWarpsPerBlock * 32)
 k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-             u32* __restrict__ t, i64* __restrict__ part) {
+             u32* __restrict__ t, i64* __restrict__ part, TriList TL) {
     __shared__ u32 s_x[kHWarpsPerBlock][32];
     __shared__ u32 s_row[kHWarpsPerBlock][32];
     __shared__ u32 s_ta[kHWarpsPerBlock][32];
@@ -177,6 +190,27 @@ k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lo
         const u32 a = items[idx];
         const u64 ub = u_begin(g, a);
         const u32 k = (u32)(g.off[a + 1] - ub);
+        if (MODE == kHPassSums && TL.rec && TL.base[idx] != kNoList) {
+            // stream the records the counting pass kept for this vertex
+            const u32 nrec = TL.n[idx];
+            if (nrec == 0) continue;
+            const uint2* rec = TL.rec + TL.base[idx];
+            if (lane < k) ta[lane] = t[g.eid[ub + lane]];
+            acc[lane] = 0;
+            __syncwarp();
+            for (u32 r = lane; r < nrec; r += 32) {
+                const uint2 rv = rec[r];
+                const u32 i = rv.x & 0xffffu, j = rv.x >> 16;
+                const u64 ti = ta[i], tj = ta[j], txy = t[rv.y];
+                atomic_add_i64(&part[2 * (u64)rv.y + 1], -(i64)(ti + tj));
+                atomicAdd(&acc[i], (unsigned long long)(tj + txy));
+                atomicAdd(&acc[j], (unsigned long long)(ti + txy));
+            }
+            __syncwarp();
+            if (lane < k && acc[lane]) atomic_add_i64(&part[2 * (u64)g.eid[ub + lane] + 1], -(i64)acc[lane]);
+            __syncwarp();
+            continue;
+        }
         u64 xb = 0, xe = 0;
         if (lane < k) {
             const u32 x = g.adj[ub + lane];
@@ -278,6 +312,37 @@ k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lo
         const u32 full = row | col;
         __syncwarp();
         rows[lane] = full;
+        if (MODE == kHPassCount && TL.rec) {
+            // keep this vertex's H-edges (i | j << 16, e) for the sums pass: exact
+            // reservation, vertices without triangles record an empty list
+            const u32 mine = __popc(row);
+            u32 pos = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const u32 o = __shfl_up_sync(0xffffffffu, pos, d);
+                if (lane >= (u32)d) pos += o;
+            }
+            const u32 nh = __shfl_sync(0xffffffffu, pos, 31);
+            unsigned long long base = 0;
+            if (lane == 0) {
+                if (nh) {
+                    base = atomicAdd(TL.count, (unsigned long long)nh);
+                    if (base + nh > TL.cap) base = kNoList;
+                }
+                TL.base[idx] = base;
+                TL.n[idx] = nh;
+            }
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base != kNoList) {
+                uint2* out = TL.rec + base + (pos - mine);
+                u32 bits = row;
+                while (bits) {
+                    const u32 j = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    *out++ = make_uint2((j << 16) | lane, s_e[wib][lane][j]);
+                }
+            }
+        }
         __syncwarp();
         // phase 2: per H-edge (lane, j > lane)
         u32 tri = 0;
@@ -374,18 +439,6 @@ __device__ u64 block_exclusive_scan64(u64* a, u32 n) {
 // One vertex a of the block H-pass.  Inlined twice, with ws = the dynamic
 // shared memory (k <= kHSmemMax: every workspace access compiles to LDS/STS/
 // ATOMS) or the block's global scratch (larger k).
-// Persistent H-edge records of the block H-pass: the counting pass appends
-// every H-edge (i | j << 16, e_xy) of vertex a to one device-wide list and
-// records (base, count) per work item; the triangle-sum pass then streams the
-// records instead of re-deriving them (base = kNoList: list full, re-derive).
-struct TriList {
-    uint2* rec;
-    u64 cap;
-    unsigned long long* count;
-    u64* base;   // per work item
-    u32* n;      // per work item
-};
-constexpr u64 kNoList = ~0ull;
 
 template <int MODE, int BLOG, typename Cand>
 __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
@@ -1370,6 +1423,8 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
                 hb += k * (k - 1) / 2; // the counting pass reserves C(k,2) records per vertex
             } else {
                 ++ls;
+                const u64 pairs = k * (k - 1) / 2; // warp pass: exact reservation, bounded here
+                hb += pairs < q ? pairs : q;
             }
             key = (cls << 12) | (log_key(q) + 1);
         }
@@ -1572,6 +1627,18 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             cs.items3b.alloc((mybig + 1) * sizeof(u32));
             cs.items3m.alloc((mymedk + 1) * sizeof(u32));
             cs.items3s.alloc((mysmall + 1) * sizeof(u32));
+            // persistent H-edge records for the sums pass (all three classes): sized
+            // once per graph from the reservation bound (C(k,2) per block vertex,
+            // min(C(k,2), s1) per warp vertex), at most ~40% of the free memory
+            if (!cs.tl_sized) {
+                size_t fr = 0, tot = 0;
+                GL_CUDA(cudaMemGetInfo(&fr, &tot));
+                cs.tl_cap = std::min<u64>(hc[19] / (u64)world + 1, (u64)(0.4 * (double)fr) / sizeof(uint2));
+                cs.tl_sized = true;
+            }
+            cs.tlist.alloc((cs.tl_cap + 1) * sizeof(uint2));
+            cs.tl_base.alloc((mybig + mymedk + mysmall + 1) * sizeof(u64));
+            cs.tl_n.alloc((mybig + mymedk + mysmall + 1) * sizeof(u32));
             if (mybig || mymedk) {
                 const u64 s1max = hc[18];
                 const u32 kmax = (u32)(hc[14] & 0xffffffffu);
@@ -1585,17 +1652,6 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const u64 hcap_l = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
                 const u64 hcap_m = std::min<u64>(s1max, 128ull * 127 / 2) + 1;
                 cs.hlist.alloc(std::max<u64>((u64)blocks_l * hcap_l, (u64)blocks_m * hcap_m) * sizeof(uint2));
-                // persistent H-edge records for the sums pass: sized once per graph from
-                // the bound sum_a min(C(k,2), s1(a)), at most ~40% of the free memory
-                if (!cs.tl_sized) {
-                    size_t fr = 0, tot = 0;
-                    GL_CUDA(cudaMemGetInfo(&fr, &tot));
-                    cs.tl_cap = std::min<u64>(hc[19] / (u64)world + 1, (u64)(0.4 * (double)fr) / sizeof(uint2));
-                    cs.tl_sized = true;
-                }
-                cs.tlist.alloc((cs.tl_cap + 1) * sizeof(uint2));
-                cs.tl_base.alloc((mybig + mymedk + 1) * sizeof(u64));
-                cs.tl_n.alloc((mybig + mymedk + 1) * sizeof(u32));
                 if (mybig) {
                     k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world,
                                                                         cs.items3b.as<u32>());
@@ -1631,8 +1687,10 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmedk, nsmall, rank, world,
                                                                       cs.items3s.as<u32>());
                 GL_LAUNCH_CHECK();
+                const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + mybig + mymedk,
+                                 cs.tl_n.as<u32>() + mybig + mymedk};
                 k_hpass_warp<kHPassCount><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
-                    g, cs.items3s.as<u32>(), mysmall, counters + 3, cs.t.as<u32>(), d_partials);
+                    g, cs.items3s.as<u32>(), mysmall, counters + 3, cs.t.as<u32>(), d_partials, TL);
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
             }
@@ -1751,8 +1809,10 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
         cs.launches += 1;
     }
     if (g.m && cs.n_items3s) {
+        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20,
+                         cs.tl_base.as<u64>() + cs.n_items3b + cs.n_items3m, cs.tl_n.as<u32>() + cs.n_items3b + cs.n_items3m};
         k_hpass_warp<kHPassSums><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
-            g, cs.items3s.as<u32>(), cs.n_items3s, counters + 6, cs.t.as<u32>(), d_partials);
+            g, cs.items3s.as<u32>(), cs.n_items3s, counters + 6, cs.t.as<u32>(), d_partials, TL);
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     }

@@ -147,6 +147,30 @@ __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
+// Guided chunked grabs from a work-list queue for warp-per-item kernels: one
+// atomic per chunk of about remaining / (4 * warps in the grid) items (1..32),
+// so millions of light items do not serialise on the queue counter.
+struct WarpGrab {
+    unsigned long long next = 0, end = 0;
+    __device__ __forceinline__ bool pop(unsigned long long* queue, u64 n_items, unsigned long long* idx) {
+        if (next == end) {
+            unsigned long long b = 0, c = 0;
+            if (lane_id() == 0) {
+                const unsigned long long seen = *(volatile unsigned long long*)queue;
+                const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+                c = seen < n_items ? (n_items - seen) / (4 * warps) : 1;
+                c = c < 1 ? 1 : (c > 32 ? 32 : c);
+                b = atomicAdd(queue, c);
+            }
+            next = __shfl_sync(0xffffffffu, b, 0);
+            end = next + __shfl_sync(0xffffffffu, c, 0);
+        }
+        if (next >= n_items) return false;
+        *idx = next++;
+        return true;
+    }
+};
+
 // Persistent H-edge records of the block H-pass: the counting pass appends
 // every H-edge (i | j << 16, e_xy) of vertex a to one device-wide list and
 // records (base, count) per work item; the triangle-sum pass then streams the
@@ -182,11 +206,9 @@ k_hpass_warp(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned lo
     u32* rows = s_row[wib];
     u32* ta = s_ta[wib];
     unsigned long long* acc = s_acc[wib];
-    for (;;) {
-        unsigned long long idx = 0;
-        if (lane == 0) idx = atomicAdd(queue, 1ull);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= n_items) break;
+    WarpGrab grab;
+    unsigned long long idx = 0;
+    while (grab.pop(queue, n_items, &idx)) {
         const u32 a = items[idx];
         const u64 ub = u_begin(g, a);
         const u32 k = (u32)(g.off[a + 1] - ub);

@@ -57,7 +57,8 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -301,7 +302,7 @@ def run_ours(args):
         pin_x7 = torch.empty(max(1, shard_n), dtype=torch.int64).pin_memory()
         pin_x10 = torch.empty(max(1, shard_n), dtype=torch.int64).pin_memory()
         e2e_ms = []
-        for i in range(args.e2e_steps + 1):
+        for i in range(args.e2e_steps + args.e2e_warmup):
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -312,9 +313,11 @@ def run_ours(args):
             g2.edge_counts(b, shard_n, pin_t.numpy().view(np.uint32)[:shard_n],
                            pin_x7.numpy().view(np.uint64)[:shard_n], pin_x10.numpy().view(np.uint64)[:shard_n])
             dt = (time.perf_counter() - t0) * 1e3
+            if os.environ.get("GL_BENCH_VERBOSE"):
+                print(f"e2e iteration {i}: {dt:.1f} ms", file=sys.stderr, flush=True)
             g2.close()
             del p2
-            if i > 0:  # first iteration is warm-up
+            if i >= args.e2e_warmup:  # warm-up iterations: first-touch allocations
                 e2e_ms.append(dt)
             assert X2 == X, "e2e counts differ from device-resident counts"
         tot = sum(e2e_ms)

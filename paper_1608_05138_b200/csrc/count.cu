@@ -847,6 +847,11 @@ __device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64
 
 constexpr int kNcBatch = 8; // b's whose window test loads are issued together
 
+#ifdef GL_CYCLE_PROF
+__device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..26] mid hash,
+                                                // [12] uniform rounds, [13] mixed rounds (dense)
+#endif
+
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
     u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin;
@@ -994,6 +999,9 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
         if (stop - k0 >= 32u) {
             // uniform stretch of full rounds inside run bs
             const u32 nfull = (stop - k0) >> 5;
+#ifdef GL_CYCLE_PROF
+            if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[12], (unsigned long long)nfull);
+#endif
             const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
             u64 acc = 0;
             // software pipeline: the next kHalf rounds' loads are in flight
@@ -1028,6 +1036,9 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             // one OR-reduction gives the bitmask of run starts inside the round,
             // from which every lane reads its run (popcount), its offset and
             // its segment (highest start at or below it)
+#ifdef GL_CYCLE_PROF
+            if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[13], 1ull);
+#endif
             const u32 k = k0 + lane;
             const bool valid = k < ke;
             const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
@@ -1110,10 +1121,6 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
         window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, cl, abase, slot_acc);
     }
 }
-
-#ifdef GL_CYCLE_PROF
-__device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..26] mid hash
-#endif
 
 template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)

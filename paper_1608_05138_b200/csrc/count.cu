@@ -1595,6 +1595,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     CountState& cs = gr.cs;
     const int sms = num_sms(gr.device);
     const u64 m = g.m, n = g.n;
+    // adjacency slots are carried as u32 in the cycle run metadata
+    if (2 * m >= (1ull << 32)) throw overflow_error("counting needs 2m < 2^32 adjacency slots (m < 2^31 edges)");
     cs.launches = 0;
     cs.began = false;
     cs.mid_done = false;

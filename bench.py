@@ -203,10 +203,18 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # GL_BENCH_SHARE_GPU=1 (test hook): every rank on cuda:0 with the gloo backend,
+    # to exercise the sharded path on a one-GPU box; production runs use NCCL, one GPU per rank
+    share = os.environ.get("GL_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:

@@ -1,0 +1,33 @@
+"""Worker for tests/test_gpu_parity.py::test_sharded_ranks_share_gpu: one rank of
+the sharded count (paper_1608_05138_b200.dist.count_sharded) with every rank on
+cuda:0 and gloo collectives, so the multi-rank path runs on a one-GPU box.
+Writes its micro-record shard and X to <out>/rank<r>.npy / .json."""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main(out_dir, scale):
+    import torch
+    import torch.distributed as dist
+    import paper_1608_05138_b200 as gl
+    from paper_1608_05138_b200.dist import count_sharded
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo")
+    g = gl.Graph.build(gl.generate_rmat(scale, 16, seed=3), 0)
+    X, (b, e) = count_sharded(g, rank, world)
+    rec = g.micro_records(b, e - b) if e > b else np.zeros(0, gl.MICRO_DTYPE)
+    np.save(os.path.join(out_dir, f"rank{rank}.npy"), rec)
+    json.dump({"X": [str(x) for x in X], "b": b, "e": e}, open(os.path.join(out_dir, f"rank{rank}.json"), "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]))

@@ -313,3 +313,27 @@ def test_cli_count_spec_examples(tmp_path):
         doc = json.loads(subprocess.run([tool, "count", str(f)], capture_output=True, text=True,
                                         check=True).stdout)
         assert [doc["counts"][f"X{i}"] for i in range(1, 18)] == d["X"][1:], name
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_ranks_share_gpu(cuda_device, tmp_path, world):
+    """The multi-rank path end to end: `world` processes (torchrun, gloo, all on
+    cuda:0) each count their cost-balanced share, exchange t / partial rows /
+    128-bit sums, and finalise their edge shard; the shards' micro records and
+    X equal the single-process count."""
+    import json
+    import subprocess
+    import sys
+    scale = 13
+    pairs = gl.generate_rmat(scale, 16, seed=3)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    worker = os.path.join(os.path.dirname(__file__), "_dist_worker.py")
+    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                    "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), worker, str(tmp_path),
+                    str(scale)], check=True, timeout=600, capture_output=True)
+    shards, xs = [], []
+    for r in range(world):
+        shards.append(np.load(tmp_path / f"rank{r}.npy"))
+        xs.append(json.load(open(tmp_path / f"rank{r}.json"))["X"])
+    assert all(x == [str(v) for v in res.X] for x in xs)
+    assert np.array_equal(np.concatenate(shards), rec)

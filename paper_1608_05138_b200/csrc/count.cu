@@ -122,10 +122,12 @@ __device__ __forceinline__ u64 u_begin(const DevGraph& g, u32 x) { return g.off[
 // member filter of the block H-pass: 2^BLOG bits (8 KB for large k, 1 KB for k <= 128)
 template <int BLOG> __device__ __forceinline__ u32 bloom_bit(u32 y) { return (y * 0x2545F491u) >> (32 - BLOG); }
 template <int BLOG> __host__ __device__ constexpr u32 bloom_words() { return (1u << BLOG) / 32; }
-// block H-pass configurations: k > 128 (512 threads, two blocks per SM) and
-// 32 < k <= 128 (128 threads, eight blocks per SM: the fixed per-vertex
-// latency of the many small vertices overlaps across blocks)
+// block H-pass configurations: k > 512 (1024 threads, one block per SM, the
+// workspace in shared memory up to k = 1088), 128 < k <= 512 (512 threads, two
+// blocks per SM) and 32 < k <= 128 (128 threads, eight blocks per SM: the
+// fixed per-vertex latency of the many small vertices overlaps across blocks)
 template <int KMAX> struct HCfg;
+template <> struct HCfg<1088> { static constexpr int THREADS = 1024, MINB = 1, BLOG = 16; };
 template <> struct HCfg<768> { static constexpr int THREADS = 512, MINB = 2, BLOG = 16; };
 template <> struct HCfg<128> { static constexpr int THREADS = 128, MINB = 8, BLOG = 13; };
 
@@ -593,7 +595,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
 #pragma unroll
             for (int u = 0; u < kHUnroll; ++u) {
                 if ((cand >> u) & 1u) {
-                    if constexpr (MODE == kHPassSums)
+                    if constexpr (sizeof(Cand) == sizeof(uint2))
                         cbuf[pos] = make_uint2(yv[u], 32u * u + lane);
                     else
                         cbuf[pos] = (unsigned short)(32u * u + lane);
@@ -607,7 +609,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
                 u32 j = 0, e = 0;
                 if (q < tot) {
                     u32 off, y;
-                    if constexpr (MODE == kHPassSums) {
+                    if constexpr (sizeof(Cand) == sizeof(uint2)) {
                         off = cbuf[q].y;
                         y = cbuf[q].x;
                     } else {
@@ -702,7 +704,9 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     // per-warp candidate buffer: (y, offset) for the sums pass; the counting
     // pass keeps offsets only (its bitmap rows need the shared memory) and
     // re-reads y from L1
-    using Cand = typename std::conditional<MODE == kHPassSums, uint2, unsigned short>::type;
+    // (the 1024-thread xl configuration keeps offsets in both modes: 48 KB static limit)
+    using Cand = typename std::conditional<MODE == kHPassSums && HCfg<KMAX>::THREADS <= 512, uint2,
+                                           unsigned short>::type;
     __shared__ Cand s_cbuf[HCfg<KMAX>::THREADS / 32][32 * kHUnroll];
     const u32 lane = lane_id();
     Cand* cbuf = s_cbuf[threadIdx.x >> 5];
@@ -1427,12 +1431,14 @@ __global__ void k_umax(DevGraph g, unsigned* __restrict__ out) {
     }
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
-// classes: 3 = k > 128 (large block), 2 = 32 < k <= 128 (small block), 1 = 2 <= k <= 32 (warp)
-__global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* __restrict__ n_large,
+// classes: 4 = k > 512 (xl block), 3 = 128 < k <= 512 (large block), 2 = 32 < k <= 128
+// (small block), 1 = 2 <= k <= 32 (warp)
+__global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* __restrict__ n_xl,
+                        unsigned long long* __restrict__ n_large,
                         unsigned long long* __restrict__ n_medium, unsigned long long* __restrict__ n_small,
                         unsigned long long* __restrict__ s1_total, unsigned long long* __restrict__ s1_max,
                         unsigned long long* __restrict__ hedge_bound) {
-    unsigned long long mx = 0, hb = 0, ll = 0, lm = 0, ls = 0, st = 0;
+    unsigned long long mx = 0, hb = 0, lx = 0, ll = 0, lm = 0, ls = 0, st = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         const u64 ub = g.off[a] + g.lcnt[a];
         const u64 k = g.off[a + 1] - ub;
@@ -1446,8 +1452,8 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
             st += q;
             u32 cls = 1;
             if (k > (u64)kHWarpMax) {
-                cls = k > 128 ? 3 : 2;
-                if (cls == 3) ++ll; else ++lm;
+                cls = k > 512 ? 4 : k > 128 ? 3 : 2;
+                if (cls == 4) ++lx; else if (cls == 3) ++ll; else ++lm;
                 mx = q > mx ? q : mx;
                 hb += k * (k - 1) / 2; // the counting pass reserves C(k,2) records per vertex
             } else {
@@ -1459,6 +1465,7 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
         }
         keys[a] = key;
     }
+    if (lx) atomicAdd(n_xl, lx);
     if (ll) atomicAdd(n_large, ll);
     if (lm) atomicAdd(n_medium, lm);
     if (ls) atomicAdd(n_small, ls);
@@ -1515,6 +1522,13 @@ __global__ void k_tiers(DevGraph g, unsigned* __restrict__ out) {
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&out[i], v);
     }
 }
+
+// counters (u64 slots after the 40 macro-sum words of cs.acc): 0 H large queue,
+// 1/2/4/7 cycle big/small/mid/small-mid queues, 3 H warp queue, 5/6/9/26 sums
+// large/warp/medium/xl queues, 8 H medium queue, 25 H xl queue, 10/11/15/16
+// cycle class counts, 12/13/21/24 H class counts (large/small/medium/xl),
+// 14 max k, 17 s1, 18 max s1, 19 H-edge bound, 20 H-edge list fill, 22-23 tiers
+constexpr int kCounters = 32;
 
 // rank's share of a cost-sorted list: sorted positions p with p % world == rank
 __global__ void k_take_rank(const u32* __restrict__ sorted, u64 begin, u64 count, int rank, int world,
@@ -1606,7 +1620,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
 
     cs.t.alloc((m + 1) * sizeof(u32));
     cs.wpre.alloc((m + 1) * sizeof(u64));
-    cs.acc.alloc(64 * sizeof(u64));
+    cs.acc.alloc(96 * sizeof(u64));
     cs.keys.alloc((std::max(m, n) + 1) * 2 * sizeof(u64)); // key in/out
     cs.items2.alloc((std::max(m, n) + 1) * 2 * sizeof(u32)); // id in/out
     const u64 plen = ((m + world - 1) / world) * (u64)world;
@@ -1615,7 +1629,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     cs.slots.alloc((2 * m + 1) * sizeof(i64));
     GL_CUDA(cudaMemsetAsync(cs.slots.p, 0, (2 * m + 1) * sizeof(i64), s));
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40; // queues + counts
-    GL_CUDA(cudaMemsetAsync(counters, 0, 24 * sizeof(u64), s));
+    GL_CUDA(cudaMemsetAsync(counters, 0, kCounters * sizeof(u64), s));
 
     Timer tm(4);
     GL_CUDA(cudaEventRecord(tm.ev[0], s));
@@ -1636,31 +1650,35 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* kout = kin + (n + 1);
             u32* iin = cs.items2.as<u32>();
             u32* iout = iin + (n + 1);
-            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 12, counters + 21, counters + 13,
-                                                        counters + 17, counters + 18, counters + 19);
+            k_hkeys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, kin, counters + 24, counters + 12, counters + 21,
+                                                        counters + 13, counters + 17, counters + 18, counters + 19);
             k_umax<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 14));
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
             cs.launches += 3 + 10;
-            u64 hc[24]; // one host round trip for all class counts and bounds
+            u64 hc[kCounters]; // one host round trip for all class counts and bounds
             GL_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
             GL_CUDA(cudaStreamSynchronize(s));
-            const u64 nbig = hc[12], nmedk = hc[21], nsmall = hc[13];
+            const u64 nxl = hc[24], nbig = hc[12], nmedk = hc[21], nsmall = hc[13];
             cs.s1 = hc[17];
             cs.work[0] = 4 * cs.s1 / (u64)world; // adjacency bytes streamed by the intersections
+            const u64 myxl = rank_share(nxl, rank, world);
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mymedk = rank_share(nmedk, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
+            cs.n_items3x = myxl;
             cs.n_items3b = mybig;
             cs.n_items3m = mymedk;
             cs.n_items3s = mysmall;
+            cs.items3x.alloc((myxl + 1) * sizeof(u32));
             cs.items3b.alloc((mybig + 1) * sizeof(u32));
             cs.items3m.alloc((mymedk + 1) * sizeof(u32));
             cs.items3s.alloc((mysmall + 1) * sizeof(u32));
-            // persistent H-edge records for the sums pass (all three classes): sized
-            // once per graph from the reservation bound (C(k,2) per block vertex,
-            // min(C(k,2), s1) per warp vertex), at most ~40% of the free memory
+            // persistent H-edge records for the sums pass (every class): sized once
+            // per graph from the reservation bound (C(k,2) per block vertex,
+            // min(C(k,2), s1) per warp vertex), at most ~40% of the free memory;
+            // headers in list order xl, large, medium, small
             if (!cs.tl_sized) {
                 size_t fr = 0, tot = 0;
                 GL_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -1668,58 +1686,58 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 cs.tl_sized = true;
             }
             cs.tlist.alloc((cs.tl_cap + 1) * sizeof(uint2));
-            cs.tl_base.alloc((mybig + mymedk + mysmall + 1) * sizeof(u64));
-            cs.tl_n.alloc((mybig + mymedk + mysmall + 1) * sizeof(u32));
-            if (mybig || mymedk) {
+            cs.tl_base.alloc((myxl + mybig + mymedk + mysmall + 1) * sizeof(u64));
+            cs.tl_n.alloc((myxl + mybig + mymedk + mysmall + 1) * sizeof(u32));
+            if (myxl || mybig || mymedk) {
                 const u64 s1max = hc[18];
                 const u32 kmax = (u32)(hc[14] & 0xffffffffu);
                 if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
-                const unsigned blocks_l = (unsigned)sms * HCfg<768>::MINB, blocks_m = (unsigned)sms * HCfg<128>::MINB;
                 cs.h_gstride = 0;
-                if (kmax > (u32)kHSmemMax) {
-                    cs.h_gstride = (hpass_ws_words(kmax, kHPassCount, bloom_words<HCfg<768>::BLOG>()) + 1) & ~1ull;
-                    cs.scratch.alloc((u64)blocks_l * cs.h_gstride * sizeof(u32));
+                if (kmax > 1088u) { // beyond the xl shared-memory workspace: per-block global scratch
+                    cs.h_gstride = (hpass_ws_words(kmax, kHPassCount, bloom_words<HCfg<1088>::BLOG>()) + 1) & ~1ull;
+                    cs.scratch.alloc((u64)sms * HCfg<1088>::MINB * cs.h_gstride * sizeof(u32));
                 }
-                const u64 hcap_l = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
+                const u64 hcap_x = std::min<u64>(s1max, (u64)kmax * (kmax - 1) / 2) + 1;
+                const u64 hcap_l = std::min<u64>(s1max, 512ull * 511 / 2) + 1;
                 const u64 hcap_m = std::min<u64>(s1max, 128ull * 127 / 2) + 1;
-                cs.hlist.alloc(std::max<u64>((u64)blocks_l * hcap_l, (u64)blocks_m * hcap_m) * sizeof(uint2));
-                if (mybig) {
-                    k_take_rank<<<grid1d(mybig, 256, sms), 256, 0, s>>>(iout, 0, nbig, rank, world,
-                                                                        cs.items3b.as<u32>());
+                cs.hlist.alloc(std::max<u64>(std::max<u64>((u64)sms * HCfg<1088>::MINB * hcap_x,
+                                                           (u64)sms * HCfg<768>::MINB * hcap_l),
+                                             (u64)sms * HCfg<128>::MINB * hcap_m) *
+                               sizeof(uint2));
+                auto launch = [&](auto kc, u64 count, u64 offset, u64 total, u32* list, u64 hbase, u64 hcap,
+                                  unsigned long long* queue) {
+                    constexpr int K = decltype(kc)::value;
+                    k_take_rank<<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
+                    const u32 kws = K == 1088 ? 1088u : (K == 768 ? 512u : 128u); // largest k of the class
                     const size_t smem =
-                        (size_t)hpass_ws_words(kHSmemMax, kHPassCount, bloom_words<HCfg<768>::BLOG>()) * sizeof(u32);
-                    smem_attr(k_hpass_block<kHPassCount, 768>, smem, gr.device);
-                    const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(),
-                                     cs.tl_n.as<u32>()};
-                    k_hpass_block<kHPassCount, 768><<<blocks_l, HCfg<768>::THREADS, smem, s>>>(
-                        g, cs.items3b.as<u32>(), mybig, counters + 0, cs.t.as<u32>(), d_partials,
-                        cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, cs.hlist.as<uint2>(), hcap_l, TL);
+                        (size_t)hpass_ws_words(kws, kHPassCount, bloom_words<HCfg<K>::BLOG>()) * sizeof(u32);
+                    smem_attr(k_hpass_block<kHPassCount, K>, smem, gr.device);
+                    const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hbase,
+                                     cs.tl_n.as<u32>() + hbase};
+                    const bool glob = K == 1088 && cs.h_gstride;
+                    k_hpass_block<kHPassCount, K><<<(unsigned)sms * HCfg<K>::MINB, HCfg<K>::THREADS, smem, s>>>(
+                        g, list, count, queue, cs.t.as<u32>(), d_partials, glob ? cs.scratch.as<u32>() : nullptr,
+                        glob ? cs.h_gstride : 0, cs.hlist.as<uint2>(), hcap, TL);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
-                }
-                if (mymedk) {
-                    k_take_rank<<<grid1d(mymedk, 256, sms), 256, 0, s>>>(iout, nbig, nmedk, rank, world,
-                                                                         cs.items3m.as<u32>());
-                    GL_LAUNCH_CHECK();
-                    const size_t smem =
-                        (size_t)hpass_ws_words(128, kHPassCount, bloom_words<HCfg<128>::BLOG>()) * sizeof(u32);
-                    smem_attr(k_hpass_block<kHPassCount, 128>, smem, gr.device);
-                    const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + mybig,
-                                     cs.tl_n.as<u32>() + mybig};
-                    k_hpass_block<kHPassCount, 128><<<blocks_m, HCfg<128>::THREADS, smem, s>>>(
-                        g, cs.items3m.as<u32>(), mymedk, counters + 8, cs.t.as<u32>(), d_partials, nullptr, 0,
-                        cs.hlist.as<uint2>(), hcap_m, TL);
-                    GL_LAUNCH_CHECK();
-                    cs.launches += 2;
-                }
+                };
+                if (myxl)
+                    launch(std::integral_constant<int, 1088>{}, myxl, 0, nxl, cs.items3x.as<u32>(), 0, hcap_x,
+                           counters + 25);
+                if (mybig)
+                    launch(std::integral_constant<int, 768>{}, mybig, nxl, nbig, cs.items3b.as<u32>(), myxl, hcap_l,
+                           counters + 0);
+                if (mymedk)
+                    launch(std::integral_constant<int, 128>{}, mymedk, nxl + nbig, nmedk, cs.items3m.as<u32>(),
+                           myxl + mybig, hcap_m, counters + 8);
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmedk, nsmall, rank, world,
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nxl + nbig + nmedk, nsmall, rank, world,
                                                                       cs.items3s.as<u32>());
                 GL_LAUNCH_CHECK();
-                const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + mybig + mymedk,
-                                 cs.tl_n.as<u32>() + mybig + mymedk};
+                const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20,
+                                 cs.tl_base.as<u64>() + myxl + mybig + mymedk, cs.tl_n.as<u32>() + myxl + mybig + mymedk};
                 k_hpass_warp<kHPassCount><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
                     g, cs.items3s.as<u32>(), mysmall, counters + 3, cs.t.as<u32>(), d_partials, TL);
                 GL_LAUNCH_CHECK();
@@ -1741,7 +1759,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
-            u64 cc[24];
+            u64 cc[kCounters];
             GL_CUDA(cudaMemcpyAsync(cc, counters, sizeof(cc), cudaMemcpyDeviceToHost, s));
             const u64 wtot = read_dev(cs.wpre.as<u64>() + m, s);
             const u64 nbig = cc[10], nmid = cc[15], nsmid = cc[16], nsmall = cc[11];
@@ -1818,30 +1836,30 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     GL_CUDA(cudaEventRecord(tm.ev[0], s));
     // triangle sums over the same vertex shares as this rank's H-pass
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40;
-    if (g.m && cs.n_items3b) {
-        const size_t smem = (size_t)hpass_ws_words(kHSmemMax, kHPassSums, bloom_words<HCfg<768>::BLOG>()) * sizeof(u32);
-        smem_attr(k_hpass_block<kHPassSums, 768>, smem, gr.device);
-        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>(), cs.tl_n.as<u32>()};
-        k_hpass_block<kHPassSums, 768><<<(unsigned)sms * HCfg<768>::MINB, HCfg<768>::THREADS, smem, s>>>(
-            g, cs.items3b.as<u32>(), cs.n_items3b, counters + 5, cs.t.as<u32>(), d_partials,
-            cs.h_gstride ? cs.scratch.as<u32>() : nullptr, cs.h_gstride, nullptr, 0, TL);
+    auto sums = [&](auto kc, u64 count, const u32* list, u64 hbase, unsigned long long* queue) {
+        constexpr int K = decltype(kc)::value;
+        const u32 kws = K == 1088 ? 1088u : (K == 768 ? 512u : 128u);
+        const size_t smem = (size_t)hpass_ws_words(kws, kHPassSums, bloom_words<HCfg<K>::BLOG>()) * sizeof(u32);
+        smem_attr(k_hpass_block<kHPassSums, K>, smem, gr.device);
+        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hbase,
+                         cs.tl_n.as<u32>() + hbase};
+        const bool glob = K == 1088 && cs.h_gstride;
+        k_hpass_block<kHPassSums, K><<<(unsigned)sms * HCfg<K>::MINB, HCfg<K>::THREADS, smem, s>>>(
+            g, list, count, queue, cs.t.as<u32>(), d_partials, glob ? cs.scratch.as<u32>() : nullptr,
+            glob ? cs.h_gstride : 0, nullptr, 0, TL);
         GL_LAUNCH_CHECK();
         cs.launches += 1;
-    }
-    if (g.m && cs.n_items3m) {
-        const size_t smem = (size_t)hpass_ws_words(128, kHPassSums, bloom_words<HCfg<128>::BLOG>()) * sizeof(u32);
-        smem_attr(k_hpass_block<kHPassSums, 128>, smem, gr.device);
-        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + cs.n_items3b,
-                         cs.tl_n.as<u32>() + cs.n_items3b};
-        k_hpass_block<kHPassSums, 128><<<(unsigned)sms * HCfg<128>::MINB, HCfg<128>::THREADS, smem, s>>>(
-            g, cs.items3m.as<u32>(), cs.n_items3m, counters + 9, cs.t.as<u32>(), d_partials, nullptr, 0, nullptr, 0,
-            TL);
-        GL_LAUNCH_CHECK();
-        cs.launches += 1;
-    }
+    };
+    if (g.m && cs.n_items3x) sums(std::integral_constant<int, 1088>{}, cs.n_items3x, cs.items3x.as<u32>(), 0, counters + 26);
+    if (g.m && cs.n_items3b)
+        sums(std::integral_constant<int, 768>{}, cs.n_items3b, cs.items3b.as<u32>(), cs.n_items3x, counters + 5);
+    if (g.m && cs.n_items3m)
+        sums(std::integral_constant<int, 128>{}, cs.n_items3m, cs.items3m.as<u32>(), cs.n_items3x + cs.n_items3b,
+             counters + 9);
     if (g.m && cs.n_items3s) {
-        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20,
-                         cs.tl_base.as<u64>() + cs.n_items3b + cs.n_items3m, cs.tl_n.as<u32>() + cs.n_items3b + cs.n_items3m};
+        const u64 hb = cs.n_items3x + cs.n_items3b + cs.n_items3m;
+        const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hb,
+                         cs.tl_n.as<u32>() + hb};
         k_hpass_warp<kHPassSums><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
             g, cs.items3s.as<u32>(), cs.n_items3s, counters + 6, cs.t.as<u32>(), d_partials, TL);
         GL_LAUNCH_CHECK();

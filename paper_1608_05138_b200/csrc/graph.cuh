@@ -77,9 +77,9 @@ struct CountState {
     u64 tl_cap = 0;
     bool tl_sized = false;
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
-    DevBuf items2, items3s, items3m, items3b; // work lists
+    DevBuf items2, items3s, items3m, items3b, items3x; // work lists
     DevBuf keys, tmp, scratch, cursor, cursor2, acc; // sort keys, cub temp, kernel scratch
-    u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0;
+    u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0, n_items3x = 0;
     u64 shard_begin = 0, shard_end = 0;
     bool have_micro = false;
     bool began = false;

@@ -28,6 +28,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -110,6 +112,7 @@ constexpr int kHWarpsPerBlock = 8;
 constexpr int kHBlockThreads = 512; // k > 32: one block per vertex
 constexpr int kHSmemMax = 768;      // k <= 768: workspace in shared memory
 constexpr int kHUnroll = 8;         // streamed rounds in flight per warp
+constexpr u32 kHProbeRatio = 8;     // probe instead of stream when |U(x_i)| > 8 * candidates
 
 __device__ __forceinline__ u64 warp_sum_u64(u64 v) {
 #pragma unroll
@@ -566,6 +569,47 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         const u64 xb = u_begin(g, x), xe = g.off[x + 1];
         u64 acc_i = 0; // kHPassSums: credit of (a, x_i), summed over the member
         const u64 ti = MODE == kHPassSums ? (u64)ta[i] : 0;
+        // one round of (hit, j = member index, e = edge id of (x_i, x_j)) with all lanes
+        auto on_hits = [&](bool hit, u32 j, u32 e) {
+            if (MODE == kHPassCount) {
+                if (hit) {
+                    atomicOr(&rows[(u64)i * RS + (j >> 5)], 1u << (j & 31));
+                    atomicOr(&rows[(u64)j * RS + (i >> 5)], 1u << (i & 31));
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                if (bal) {
+                    u32 base = 0;
+                    if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (hit) hout[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
+                }
+            } else if (hit) {
+                const u64 txy = t[e];
+                const u64 tj = ta[j];
+                atomic_add_i64(&part[2 * (u64)e + 1], -(i64)(ti + tj));
+                acc_i += tj + txy;
+                atomicAdd(&acc[j], (unsigned long long)(ti + txy));
+            }
+        };
+        const u32 rem = k - 1 - i;
+        if (xe - xb > (u64)kHProbeRatio * rem) {
+            // U(x_i) much longer than the candidates x_j (j > i): probe each
+            // candidate with a binary search instead of streaming the list
+            for (u32 j0 = i + 1; j0 < k; j0 += 32) {
+                const u32 j = j0 + lane;
+                bool hit = false;
+                u32 e = 0;
+                if (j < k) {
+                    const u32 y = xs[j];
+                    const u64 pp = lower_bound_dev<u32, u64>(g.adj, xb, xe, y);
+                    if (pp < xe && g.adj[pp] == y) {
+                        hit = true;
+                        e = g.eid[pp];
+                    }
+                }
+                on_hits(hit, j, e);
+            }
+        } else
         for (u64 p0 = xb; p0 < xe; p0 += 32u * kHUnroll) {
             // kHUnroll coalesced rounds in flight; Bloom-filter them, then
             // compact the candidates into the warp's buffer so that the
@@ -629,25 +673,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
                     }
                     if (hit) e = g.eid[p0 + off];
                 }
-                if (MODE == kHPassCount) {
-                    if (hit) {
-                        atomicOr(&rows[(u64)i * RS + (j >> 5)], 1u << (j & 31));
-                        atomicOr(&rows[(u64)j * RS + (i >> 5)], 1u << (i & 31));
-                    }
-                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                    if (bal) {
-                        u32 base = 0;
-                        if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (hit) hout[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
-                    }
-                } else if (hit) {
-                    const u64 txy = t[e];
-                    const u64 tj = ta[j];
-                    atomic_add_i64(&part[2 * (u64)e + 1], -(i64)(ti + tj));
-                    acc_i += tj + txy;
-                    atomicAdd(&acc[j], (unsigned long long)(ti + txy));
-                }
+                on_hits(hit, j, e);
             }
             __syncwarp();
         }
@@ -1445,9 +1471,10 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
         u32 key = 0;
         if (k >= 2) {
             u64 q = 0;
-            for (u64 i = 0; i + 1 < k; ++i) {
+            for (u64 i = 0; i + 1 < k; ++i) { // entries read: streamed list or ~8 per probe
                 const u32 x = g.adj[ub + i];
-                q += g.off[x + 1] - (g.off[x] + g.lcnt[x]);
+                const u64 ul = g.off[x + 1] - (g.off[x] + g.lcnt[x]), pr = (u64)kHProbeRatio * (k - 1 - i);
+                q += ul < pr ? ul : pr;
             }
             st += q;
             u32 cls = 1;
@@ -1661,6 +1688,11 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             GL_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
             GL_CUDA(cudaStreamSynchronize(s));
             const u64 nxl = hc[24], nbig = hc[12], nmedk = hc[21], nsmall = hc[13];
+            if (std::getenv("GL_DEBUG"))
+                std::fprintf(stderr, "[gl] H-pass classes xl %llu large %llu medium %llu small %llu, kmax %llu, s1 %llu\n",
+                             (unsigned long long)nxl, (unsigned long long)nbig, (unsigned long long)nmedk,
+                             (unsigned long long)nsmall, (unsigned long long)(hc[14] & 0xffffffffu),
+                             (unsigned long long)hc[17]);
             cs.s1 = hc[17];
             cs.work[0] = 4 * cs.s1 / (u64)world; // adjacency bytes streamed by the intersections
             const u64 myxl = rank_share(nxl, rank, world);

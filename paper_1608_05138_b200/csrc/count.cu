@@ -882,9 +882,26 @@ __device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..2
                                                 // [12] uniform rounds, [13] mixed rounds (dense)
 #endif
 
+// First index in [lo, hi) with a[idx] >= x, searching outward from a hint
+// (the previous window's run end of the same row): a doubling probe towards
+// the answer from the hint, then a binary search -- ~2 log2 |error| loads.
+__device__ __forceinline__ u64 gallop_from(const u32* __restrict__ a, u64 lo, u64 hi, u64 hint, u32 x) {
+    if (hint <= lo || hint >= hi) return gallop_lower_bound(a, lo, hi, x);
+    if (a[hint] < x) return gallop_lower_bound(a, hint + 1, hi, x);
+    // answer in [lo, hint]: double backwards
+    u64 r = hint, step = 1;
+    for (;;) {
+        if (r < lo + step) return lower_bound_dev<u32, u64>(a, lo, r, x);
+        const u64 p = r - step;
+        if (a[p] < x) return lower_bound_dev<u32, u64>(a, p + 1, r, x);
+        r = p;
+        step <<= 1;
+    }
+}
+
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
-    u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin;
+    u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin, *plen;
     u64* rb;
 };
 // compacted runs of one window: wedge prefix pre[nnz+1], first adjacency slot
@@ -904,9 +921,10 @@ __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     s.rb = reinterpret_cast<u64*>(base + ((6 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
     s.nextc = reinterpret_cast<u32*>(s.rb + cap); // c at the cursor (kEmpty: row done)
     s.rwin = s.nextc + cap;                        // window of b's last recorded run
+    s.plen = s.rwin + cap;                         // length of b's last run (search hint)
     return s;
 }
-__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 10ull * cap + 8; }
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 11ull * cap + 8; }
 
 
 // W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
@@ -1029,7 +1047,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
         if (stop - k0 >= 32u) {
             // uniform stretch of full rounds inside run bs
             const u32 nfull = (stop - k0) >> 5;
-#ifdef GL_CYCLE_PROF
+#ifdef GL_CYCLE_PROF_ROUNDS
             if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[12], (unsigned long long)nfull);
 #endif
             const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
@@ -1066,7 +1084,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             // one OR-reduction gives the bitmask of run starts inside the round,
             // from which every lane reads its run (popcount), its offset and
             // its segment (highest start at or below it)
-#ifdef GL_CYCLE_PROF
+#ifdef GL_CYCLE_PROF_ROUNDS
             if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[13], 1ull);
 #endif
             const u32 k = k0 + lane;
@@ -1213,6 +1231,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             const u32 c = re > 0 ? g.adj[rb] : kEmpty;
             S.nextc[j] = c;
             S.rwin[j] = kEmpty;
+            S.plen[j] = 0;
             if (!HASH && c != kEmpty) atomicMin(&s_next, c);
         }
         __syncthreads();
@@ -1251,7 +1270,12 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                     const u32 j = j0 + u * THREADS;
                     const u32 c0 = S.cur[j], re = S.rend[j];
                     const u64 rb = S.rb[j];
-                    const u32 h = HASH ? re : (u32)(gallop_lower_bound(g.adj, rb + c0, rb + re, hi) - rb);
+                    u32 h = re;
+                    if (!HASH) {
+                        const u32 pl = S.plen[j];
+                        h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
+                        S.plen[j] = h - c0;
+                    }
                     S.hpos[j] = c0; // run start
                     S.rwin[j] = win;
                     S.cur[j] = h;

@@ -848,6 +848,23 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
 // to per-adjacency-slot accumulators (consecutive wedges of a run are
 // consecutive slots), folded into edge rows by k_fold_slots.
 
+// Shared-space access with a 32-bit address computed once per kernel (the
+// generic-pointer form re-derives the shared window base per access).
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void red_shared_add(u32 addr, u32 v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ u32 ld_shared(u32 addr) {
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// RED.ADD.U64 to global issued under a predicate (no branch around it)
+__device__ __forceinline__ void red_add_u64_if(i64* p, u64 v) {
+    asm volatile("{ .reg .pred q; setp.ne.u64 q, %1, 0; @q red.global.add.u64 [%0], %1; }" ::"l"(p), "l"(v)
+                 : "memory");
+}
+
 // Packed window counters: 2^cl counters of (32 >> cl) bits per word.  The
 // width follows the degree tier of the window's c ids (internal ids ascend
 // with degree): W_a[c] <= deg(c), so ids with degree < 4 take 2-bit counters,
@@ -992,6 +1009,22 @@ __device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, u32 cl) { W
 template <int KIND, int PASS>
 __device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, u32 cl, i64* __restrict__ slot_acc, u64 slot,
                                          u64& val) {
+    if (!Cyc<KIND>::HASH) { // dense window: 32-bit shared addresses, predicated RED
+        const u32 ci = cv - lo;
+        const u32 addr = smem_u32(W) + ((ci >> cl) << 2);
+        const u32 sh = (ci & ((1u << cl) - 1u)) << (5 - cl);
+        if (PASS == 0) {
+            red_shared_add(addr, 1u << sh);
+        } else if (PASS == 1) {
+            const u32 w = ld_shared(addr) >> sh;
+            const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
+            red_add_u64_if(&slot_acc[slot], (u64)v);
+            val = v;
+        } else {
+            W[ci >> cl] = 0;
+        }
+        return;
+    }
     if (PASS == 0) {
         tab_inc<KIND>(W, cv, lo, cl);
     } else if (PASS == 1) {

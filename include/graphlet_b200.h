@@ -165,6 +165,11 @@ int gl_edge_counts(const gl_graph *g, uint64_t first, uint64_t count, uint32_t *
 int gl_edge_counts_device(const gl_graph *g, const uint32_t **t, const uint64_t **x7,
                           const uint64_t **x10);
 
+/* The cycle pass runs on its own stream concurrently with the clique /
+ * triangle pass (default 1); 0 serialises them on the caller's stream, e.g.
+ * to time each pass alone. Process-wide. */
+int gl_set_overlap(int on);
+
 /* Kernel timing of the last count call (CUDA events on the launching stream),
  * milliseconds: [0] clique+triangle pass, [1] triangle sums, [2] cycles,
  * [3] epilogue+macro reduction, [4] total.  Launch count in *launches. */

@@ -113,6 +113,11 @@ uint64_t gl_last_error_line(void) { return t_line; }
 const char* gl_version(void) { return "graphlet_b200 0.1 (sm_100a)"; }
 void gl_free(void* p) { std::free(p); }
 
+int gl_set_overlap(int on) {
+    gl::g_overlap.store(on ? 1 : 0);
+    return GL_OK;
+}
+
 int gl_trim_device_cache(void) {
     return guarded([&] { gl::pool_trim(); });
 }

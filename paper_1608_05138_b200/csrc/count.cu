@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -1684,6 +1685,8 @@ u64 rank_share(u64 count, int rank, int world) {
 
 } // namespace
 
+std::atomic<int> g_overlap{1}; // run the cycle pass concurrently with the H-pass (gl_set_overlap)
+
 // Phase A: H-pass (t and x7 partials) and the cycle kernels (C4 into y).
 void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s) {
     GL_CUDA(cudaSetDevice(gr.device));
@@ -1715,10 +1718,20 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40; // queues + counts
     GL_CUDA(cudaMemsetAsync(counters, 0, kCounters * sizeof(u64), s));
 
-    Timer tm(4);
-    GL_CUDA(cudaEventRecord(tm.ev[0], s));
+    // The H-pass (stream s) and the cycle pass (cs.s2, forked after the wedge
+    // prefix) are independent and run concurrently; count_mid joins them.
+    if (cs.s2) GL_CUDA(cudaStreamSynchronize(cs.s2)); // a previous, un-joined cycle pass
+    if (!cs.s2) {
+        GL_CUDA(cudaStreamCreateWithFlags(&cs.s2, cudaStreamNonBlocking));
+        for (int i = 0; i < 8; ++i) GL_CUDA(cudaEventCreate(&cs.ev[i]));
+    }
+    cudaStream_t s2 = g_overlap.load() ? cs.s2 : s; // serial mode: everything on s
+    cs.keys_c.alloc((n + 1) * 2 * sizeof(u32));
+    cs.items_c.alloc((n + 1) * 2 * sizeof(u32));
+    GL_CUDA(cudaEventRecord(cs.ev[0], s));
     if (m == 0) {
-        for (int i = 1; i < 3; ++i) GL_CUDA(cudaEventRecord(tm.ev[i], s));
+        for (int i = 1; i < 4; ++i) GL_CUDA(cudaEventRecord(cs.ev[i], s));
+        GL_CUDA(cudaEventRecord(cs.ev[6], s)); // fork/join point of the (empty) cycle pass
     } else {
         u64* wedges = cs.keys.as<u64>(); // scratch reuse before the sorts
         k_prepass<<<grid1d(m, 256, sms), 256, 0, s>>>(g, wedges);
@@ -1726,6 +1739,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
         GL_CUDA(cudaMemsetAsync(wedges + m, 0, sizeof(u64), s));
         dev_exclusive_scan<u64>(cs.tmp, wedges, cs.wpre.as<u64>(), m + 1, s);
         cs.launches += 2;
+        GL_CUDA(cudaEventRecord(cs.ev[6], s)); // fork: the cycle pass needs the wedge prefix only
+        GL_CUDA(cudaStreamWaitEvent(s2, cs.ev[6], 0));
 
         // H-pass: vertices by streaming cost descending; k > 32 block kernel, else warp kernel.
         // The rank's lists stay in items3b / items3s for the triangle-sum pass (count_mid).
@@ -1833,24 +1848,24 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 cs.launches += 2;
             }
         }
-        GL_CUDA(cudaEventRecord(tm.ev[1], s));
-        GL_CUDA(cudaEventRecord(tm.ev[2], s));
+        GL_CUDA(cudaEventRecord(cs.ev[1], s));
 
         // cycles: top vertices, split small (warp hash) / big (block windows)
+        GL_CUDA(cudaEventRecord(cs.ev[2], s2));
         {
-            u32* kin = cs.keys.as<u32>();
+            u32* kin = cs.keys_c.as<u32>();
             u32* kout = kin + (n + 1);
-            u32* iin = cs.items2.as<u32>();
+            u32* iin = cs.items_c.as<u32>();
             u32* iout = iin + (n + 1);
-            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,
+            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,
                                                            counters + 16, counters + 11);
-            k_tiers<<<grid1d(n, 256, sms), 256, 0, s>>>(g, (unsigned*)(counters + 22));
-            k_seq<<<grid1d(n, 256, sms), 256, 0, s>>>(iin, n);
+            k_tiers<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, (unsigned*)(counters + 22));
+            k_seq<<<grid1d(n, 256, sms), 256, 0, s2>>>(iin, n);
             GL_LAUNCH_CHECK();
-            dev_sort_desc(cs.tmp, kin, kout, iin, iout, n, s);
+            dev_sort_desc(cs.tmp_c, kin, kout, iin, iout, n, s2);
             u64 cc[kCounters];
-            GL_CUDA(cudaMemcpyAsync(cc, counters, sizeof(cc), cudaMemcpyDeviceToHost, s));
-            const u64 wtot = read_dev(cs.wpre.as<u64>() + m, s);
+            GL_CUDA(cudaMemcpyAsync(cc, counters, sizeof(cc), cudaMemcpyDeviceToHost, s2));
+            const u64 wtot = read_dev(cs.wpre.as<u64>() + m, s2);
             const u64 nbig = cc[10], nmid = cc[15], nsmid = cc[16], nsmall = cc[11];
             const uint4 tiers = make_uint4((u32)cc[22], (u32)(cc[22] >> 32), (u32)cc[23], (u32)(cc[23] >> 32));
             cs.work[2] = 12 * wtot / (u64)world; // 4 B c id + 8 B slot credit per wedge
@@ -1877,11 +1892,11 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     constexpr int K = decltype(kind)::value;
                     const u32 cap = K == 0 ? cap_big : cap_hash;
                     u32* scratch = K == 0 ? cs.cursor.as<u32>() : cs.cursor2.as<u32>();
-                    k_take_rank<<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
+                    k_take_rank<<<grid1d(count, 256, sms), 256, 0, s2>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
                     smem_attr(k_cycle_block<K>, smem, gr.device);
-                    k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s>>>(
+                    k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s2>>>(
                         g, list, count, queue, cs.slots.as<i64>(), scratch, cap, tiers);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
@@ -1891,24 +1906,18 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 if (mysmid) launch(std::integral_constant<int, 2>{}, lsmid, mysmid, nbig + nmid, nsmid, counters + 7);
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nbig + nmid + nsmid, nsmall, rank, world, lsmall);
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s2>>>(iout, nbig + nmid + nsmid, nsmall, rank, world, lsmall);
                 GL_LAUNCH_CHECK();
                 const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
                 smem_attr(k_cycle_small, smem, gr.device);
-                k_cycle_small<<<(unsigned)sms * 3, kCycleSmallWarps * 32, smem, s>>>(
+                k_cycle_small<<<(unsigned)sms * 3, kCycleSmallWarps * 32, smem, s2>>>(
                     g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, cs.slots.as<i64>());
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
             }
-            k_fold_slots<<<grid1d(m, 256, sms), 256, 0, s>>>(g, cs.slots.as<i64>(), d_partials);
-            GL_LAUNCH_CHECK();
-            cs.launches += 1;
         }
     }
-    GL_CUDA(cudaEventRecord(tm.ev[3], s));
-    GL_CUDA(cudaEventSynchronize(tm.ev[3]));
-    GL_CUDA(cudaEventElapsedTime(&cs.ms[0], tm.ev[0], tm.ev[1]));
-    GL_CUDA(cudaEventElapsedTime(&cs.ms[2], tm.ev[2], tm.ev[3]));
+    if (m) GL_CUDA(cudaEventRecord(cs.ev[3], s2)); // cycle pass done
     cs.ms[1] = 0;
     cs.began = true;
 }
@@ -1921,8 +1930,7 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     if (!cs.began) throw state_error("gl_count_mid before gl_count_begin");
     const DevGraph& g = gr.d;
     const int sms = num_sms(gr.device);
-    Timer tm(2);
-    GL_CUDA(cudaEventRecord(tm.ev[0], s));
+    GL_CUDA(cudaEventRecord(cs.ev[4], s));
     // triangle sums over the same vertex shares as this rank's H-pass
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40;
     auto sums = [&](auto kc, u64 count, const u32* list, u64 hbase, unsigned long long* queue) {
@@ -1955,9 +1963,15 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
         cs.launches += 1;
     }
     cs.work[1] = cs.work[0];
-    GL_CUDA(cudaEventRecord(tm.ev[1], s));
-    GL_CUDA(cudaEventSynchronize(tm.ev[1]));
-    GL_CUDA(cudaEventElapsedTime(&cs.ms[1], tm.ev[0], tm.ev[1]));
+    GL_CUDA(cudaEventRecord(cs.ev[5], s));
+    // join the cycle pass, then fold its per-slot C4 credits into the y rows
+    // (after the sums: both update y, the fold non-atomically)
+    GL_CUDA(cudaStreamWaitEvent(s, cs.ev[3], 0));
+    if (g.m) {
+        k_fold_slots<<<grid1d(g.m, 256, sms), 256, 0, s>>>(g, cs.slots.as<i64>(), d_partials);
+        GL_LAUNCH_CHECK();
+        cs.launches += 1;
+    }
     cs.mid_done = true;
 }
 
@@ -1988,6 +2002,11 @@ void count_finish(Graph& gr, const i64* d_part_shard, u64 begin, u64 end, u128 C
     GL_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, s));
     GL_CUDA(cudaStreamSynchronize(s));
     GL_CUDA(cudaEventElapsedTime(&cs.ms[3], tm.ev[0], tm.ev[1]));
+    // phase times of begin/mid (their events completed before this sync):
+    // H-pass, triangle sums, cycle pass (concurrent with the other two)
+    GL_CUDA(cudaEventElapsedTime(&cs.ms[0], cs.ev[0], cs.ev[1]));
+    GL_CUDA(cudaEventElapsedTime(&cs.ms[1], cs.ev[4], cs.ev[5]));
+    GL_CUDA(cudaEventElapsedTime(&cs.ms[2], cs.ev[2], cs.ev[3]));
     cs.ms[4] = cs.ms[0] + cs.ms[1] + cs.ms[2] + cs.ms[3];
     cs.work[3] = 52 * (end - begin); // t,x7,y,eu,ev,2 degrees in; x7,x10 out
     const unsigned* flags = reinterpret_cast<const unsigned*>(h + 36);

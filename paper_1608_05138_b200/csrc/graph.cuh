@@ -15,6 +15,8 @@
 //   deg   u32[n], label u64[n]
 #pragma once
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace gl {
@@ -79,6 +81,9 @@ struct CountState {
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3m, items3b, items3x; // work lists
     DevBuf keys, tmp, scratch, cursor, cursor2, acc; // sort keys, cub temp, kernel scratch
+    DevBuf keys_c, items_c, tmp_c; // the cycle pass's own (it runs concurrently on s2)
+    cudaStream_t s2 = nullptr;     // cycle-pass stream (owned)
+    cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork
     u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0, n_items3x = 0;
     u64 shard_begin = 0, shard_end = 0;
     bool have_micro = false;
@@ -98,6 +103,12 @@ struct Graph {
     DevBuf b_off, b_adj, b_eid, b_lcnt, b_loff, b_ev, b_eu, b_epos, b_deg, b_label;
     CountState cs;
     ~Graph() {
+        if (cs.s2) {
+            cudaStreamSynchronize(cs.s2);
+            for (auto e : cs.ev)
+                if (e) cudaEventDestroy(e);
+            cudaStreamDestroy(cs.s2);
+        }
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -107,6 +118,7 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device);
 void generate_rmat_device(const RmatParams& p, u64 count, u64* d_pairs, cudaStream_t s);
 
 // count.cu
+extern std::atomic<int> g_overlap;
 void count_begin(Graph& g, int rank, int world, i64* d_partials, cudaStream_t s);
 void count_mid(Graph& g, i64* d_partials, cudaStream_t s);
 void count_finish(Graph& g, const i64* d_partials, u64 begin, u64 end, u128 C[17],

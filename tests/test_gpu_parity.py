@@ -125,10 +125,11 @@ def test_edge_cases(cuda_device):
     assert sorted(g.labels().tolist()) == sorted({0, 3, 10**15, 2**64 - 1})
 
 
-@pytest.mark.parametrize("n", [5, 12, 40, 600, 800])
+@pytest.mark.parametrize("n", [5, 12, 40, 600, 800, 1000, 1200])
 def test_complete_graphs_closed_form(cuda_device, n):
     """K_n: X3=C(n,3), X7=C(n,4); per edge t=n-2, x7=C(n-2,2), x10=0.
-    K_800 drives |U(a)| = 799 > the 768-member shared-memory H_a stage (global path)."""
+    |U(a)| = n-1-a covers every H-pass class: K_800/K_1000 the xl class in
+    shared memory, K_1200 (|U(0)| = 1199 > 1088) its global-scratch path."""
     pairs = [(a, b) for a in range(n) for b in range(a + 1, n)]
     g, res, rec = gpu_count(pairs, cuda_device)
     X = res.X

@@ -146,7 +146,7 @@ __host__ __device__ inline u64 hpass_ws_words(u32 k, int mode, u32 bloom_w) {
     const u64 W = (k + 31) / 32;
     const u64 body = mode == 0 ? 2ull * k + (u64)k * (W | 1)  // xs, tri, rows (odd stride)
                                : 4ull * k + 2;          // xs, ta, acc (u64, aligned)
-    return body + 2 + H + H / 2 + bloom_w;
+    return body + 2 + H + H / 2 + bloom_w + 2ull * k; // + member list bounds
 }
 
 __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
@@ -523,8 +523,13 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     u32* bloom = ws + body;
     u32* hkey = bloom + bloom_words<BLOG>();
     unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
+    u32* mb = hkey + H + H / 2; // member list bounds U(x_i) = [mb, me): loaded once,
+    u32* me = mb + k;           // in parallel, instead of per member in phase 1
     for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-        xs[i] = g.adj[ub + i];
+        const u32 x = g.adj[ub + i];
+        xs[i] = x;
+        mb[i] = (u32)u_begin(g, x);
+        me[i] = (u32)g.off[x + 1];
         if (MODE == kHPassCount) {
             tri[i] = 0;
         } else {
@@ -566,8 +571,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         if (lane == 0) i = atomicAdd(&s_mi, 1u);
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i + 1 >= k) break;
-        const u32 x = xs[i];
-        const u64 xb = u_begin(g, x), xe = g.off[x + 1];
+        const u64 xb = mb[i], xe = me[i];
         u64 acc_i = 0; // kHPassSums: credit of (a, x_i), summed over the member
         const u64 ti = MODE == kHPassSums ? (u64)ta[i] : 0;
         // one round of (hit, j = member index, e = edge id of (x_i, x_j)) with all lanes

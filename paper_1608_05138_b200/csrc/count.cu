@@ -1526,18 +1526,24 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
                         unsigned long long* __restrict__ n_medium, unsigned long long* __restrict__ n_small,
                         unsigned long long* __restrict__ s1_total, unsigned long long* __restrict__ s1_max,
                         unsigned long long* __restrict__ hedge_bound) {
+    // one warp per vertex: lanes split the members (the cost sum over a hub's
+    // members is a chain of dependent loads for a single thread)
     unsigned long long mx = 0, hb = 0, lx = 0, ll = 0, lm = 0, ls = 0, st = 0;
-    for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
+    const u32 lane = lane_id();
+    const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nwarp = ((u64)gridDim.x * blockDim.x) >> 5;
+    for (u64 a = warp; a < g.n; a += nwarp) {
         const u64 ub = g.off[a] + g.lcnt[a];
         const u64 k = g.off[a + 1] - ub;
+        u64 q = 0;
+        for (u64 i = lane; i + 1 < k; i += 32) { // entries read: streamed list or ~8 per probe
+            const u32 x = g.adj[ub + i];
+            const u64 ul = g.off[x + 1] - (g.off[x] + g.lcnt[x]), pr = (u64)kHProbeRatio * (k - 1 - i);
+            q += ul < pr ? ul : pr;
+        }
+        q = warp_sum_u64(q);
+        if (lane) continue;
         u32 key = 0;
         if (k >= 2) {
-            u64 q = 0;
-            for (u64 i = 0; i + 1 < k; ++i) { // entries read: streamed list or ~8 per probe
-                const u32 x = g.adj[ub + i];
-                const u64 ul = g.off[x + 1] - (g.off[x] + g.lcnt[x]), pr = (u64)kHProbeRatio * (k - 1 - i);
-                q += ul < pr ? ul : pr;
-            }
             st += q;
             u32 cls = 1;
             if (k > (u64)kHWarpMax) {

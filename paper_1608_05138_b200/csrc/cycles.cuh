@@ -1,0 +1,647 @@
+// cycles.cuh -- the 4-cycle pass kernels: per top vertex a (Chiba-Nishizeki
+// wedges a-b-c, b < a, c < a), W_a[c] in degree-tiered dense shared-memory
+// windows (big tops) or block / warp hashes (smaller tops), C4 credits to
+// adjacency-slot accumulators.  Included by count.cu inside gl::<anonymous>.
+#pragma once
+
+// ------------------------------------------------------------------ cycles
+
+__device__ __forceinline__ u32 hslot(u32 key) { return (key * 0x9E3779B1u) >> (32 - 10); }
+static_assert(kHashSlots == 1024, "hslot assumes 1024 slots");
+
+// Small tops: one warp per top vertex a, W[c] in a warp-private hash.
+__global__ void __launch_bounds__(kCycleSmallWarps * 32)
+k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ items, u64 n_items,
+              unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc) {
+    extern __shared__ u32 smem[];
+    const u32 lane = lane_id();
+    const u32 wib = threadIdx.x >> 5;
+    u32* keys = smem + wib * 2 * kHashSlots;
+    u32* cnt = keys + kHashSlots;
+    for (u32 i = lane; i < kHashSlots; i += 32) {
+        keys[i] = kEmpty;
+        cnt[i] = 0;
+    }
+    __syncwarp();
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(queue, 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= n_items) break;
+        const u32 a = items[idx];
+        const u64 E0 = g.loff[a], E1 = g.loff[a + 1];
+        const u64 w0 = wpre[E0], w1 = wpre[E1];
+        const u32 nw = (u32)(w1 - w0);
+        // pass 1: W[c]++
+        for (u32 base = 0; base < nw; base += 32) {
+            u32 k = base + lane;
+            if (k < nw) {
+                u64 gi = w0 + k;
+                u64 e = upper_bound_dev<u64, u64>(wpre, E0, E1 + 1, gi) - 1;
+                u32 b = g.eu[e];
+                u32 cv = g.adj[g.off[b] + (gi - wpre[e])];
+                u32 h = hslot(cv);
+                for (;;) {
+                    u32 prev = atomicCAS(&keys[h], kEmpty, cv);
+                    if (prev == kEmpty || prev == cv) break;
+                    h = (h + 1) & (kHashSlots - 1);
+                }
+                atomicAdd(&cnt[h], 1u);
+            }
+        }
+        __syncwarp();
+        // pass 2: credit W[c]-1 to (b,c) and, summed per b, to (a,b)
+        for (u32 base = 0; base < nw; base += 32) {
+            u32 k = base + lane;
+            u64 e = ~0ull, val = 0;
+            if (k < nw) {
+                u64 gi = w0 + k;
+                e = upper_bound_dev<u64, u64>(wpre, E0, E1 + 1, gi) - 1;
+                u32 b = g.eu[e];
+                u64 slot = g.off[b] + (gi - wpre[e]);
+                u32 cv = g.adj[slot];
+                u32 h = hslot(cv);
+                while (keys[h] != cv) h = (h + 1) & (kHashSlots - 1);
+                val = cnt[h] - 1;
+                if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
+            }
+            u64 sum;
+            bool tail = seg_tail_sum(e, val, &sum);
+            if (k < nw && tail && sum) atomic_add_i64(&slot_acc[g.off[a] + (e - E0)], (i64)sum);
+        }
+        __syncwarp();
+        for (u32 i = lane; i < kHashSlots; i += 32) {
+            keys[i] = kEmpty;
+            cnt[i] = 0;
+        }
+        __syncwarp();
+    }
+}
+
+// Big tops: one block per top vertex a, dense W windows over c in shared
+// memory (16-bit packed counters when |L(a)| < 65536: 64K c-values per
+// window, else 32-bit: 32K).  Per window the non-empty runs
+// N(b) n [lo,hi) of the lower neighbours b are compacted (flag scan) and
+// prefix-summed in per-block global scratch; the wedges are then flattened
+// block-wide: each warp takes rounds of 32 consecutive wedges, finds the
+// round's first run with one warp-uniform binary search and each lane's run
+// among the next 32 (all non-empty) with a 5-step shuffle search.  Credits go
+// to per-adjacency-slot accumulators (consecutive wedges of a run are
+// consecutive slots), folded into edge rows by k_fold_slots.
+
+// Shared-space access with a 32-bit address computed once per kernel (the
+// generic-pointer form re-derives the shared window base per access).
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void red_shared_add(u32 addr, u32 v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ u32 ld_shared(u32 addr) {
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// RED.ADD.U64 to global issued under a predicate (no branch around it)
+__device__ __forceinline__ void red_add_u64_if(i64* p, u64 v) {
+    asm volatile("{ .reg .pred q; setp.ne.u64 q, %1, 0; @q red.global.add.u64 [%0], %1; }" ::"l"(p), "l"(v)
+                 : "memory");
+}
+
+// Packed window counters: 2^cl counters of (32 >> cl) bits per word.  The
+// width follows the degree tier of the window's c ids (internal ids ascend
+// with degree): W_a[c] <= deg(c), so ids with degree < 4 take 2-bit counters,
+// < 16 4-bit, < 256 8-bit, < 65536 16-bit, the rest 32-bit -- the window over
+// low-degree ids is up to 16x wider than a 32-bit one.
+__device__ __forceinline__ void w_inc(u32* W, u32 i, u32 cl) {
+    atomicAdd(&W[i >> cl], 1u << ((i & ((1u << cl) - 1u)) << (5 - cl)));
+}
+__device__ __forceinline__ u32 w_get(const u32* W, u32 i, u32 cl) {
+    const u32 v = W[i >> cl] >> ((i & ((1u << cl) - 1u)) << (5 - cl));
+    return cl == 0 ? v : v & ((1u << (32u >> cl)) - 1u);
+}
+
+// first index in [lo, hi) with a[idx] >= x, galloping from lo: runs inside a
+// window are usually a handful of entries, so this costs ~log2(run) loads.
+__device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64 lo, u64 hi, u32 x) {
+    if (lo >= hi || a[lo] >= x) return lo;
+    u64 step = 1, base = lo;
+    for (;;) {
+        const u64 probe = base + step;
+        if (probe >= hi) return lower_bound_dev<u32, u64>(a, base + 1, hi, x);
+        if (a[probe] >= x) return lower_bound_dev<u32, u64>(a, base + 1, probe, x);
+        base = probe;
+        step <<= 1;
+    }
+}
+
+constexpr int kNcBatch = 8; // b's whose window test loads are issued together
+
+#ifdef GL_CYCLE_PROF
+__device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..26] mid hash,
+                                                // [12] uniform rounds, [13] mixed rounds (dense)
+#endif
+
+// First index in [lo, hi) with a[idx] >= x, searching outward from a hint
+// (the previous window's run end of the same row): a doubling probe towards
+// the answer from the hint, then a binary search -- ~2 log2 |error| loads.
+__device__ __forceinline__ u64 gallop_from(const u32* __restrict__ a, u64 lo, u64 hi, u64 hint, u32 x) {
+    if (hint <= lo || hint >= hi) return gallop_lower_bound(a, lo, hi, x);
+    if (a[hint] < x) return gallop_lower_bound(a, hint + 1, hi, x);
+    // answer in [lo, hint]: double backwards
+    u64 r = hint, step = 1;
+    for (;;) {
+        if (r < lo + step) return lower_bound_dev<u32, u64>(a, lo, r, x);
+        const u64 p = r - step;
+        if (a[p] < x) return lower_bound_dev<u32, u64>(a, p + 1, r, x);
+        r = p;
+        step <<= 1;
+    }
+}
+
+// per-block scratch layout (cap = dmax + 2 entries each, cap even)
+struct BigScratch {
+    u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin, *plen;
+    u64* rb;
+};
+// compacted runs of one window: wedge prefix pre[nnz+1], first adjacency slot
+// rs[q] (u32: 2m < 2^32 is checked on the host), lower-neighbour index rj[q];
+// in shared memory when nnz fits, else in the block's global scratch
+struct RunMeta {
+    u32 *pre, *rs, *rj;
+};
+__device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
+    BigScratch s;
+    s.cur = base;
+    s.hpos = base + cap;
+    s.rend = base + 2 * (u64)cap;
+    s.pre = base + 3 * (u64)cap;              // cap + 1 entries
+    s.rj = base + 4 * (u64)cap + 1;
+    s.rs = base + 5 * (u64)cap + 1;
+    s.rb = reinterpret_cast<u64*>(base + ((6 * (u64)cap + 2) & ~1ull)); // 8B aligned (base is)
+    s.nextc = reinterpret_cast<u32*>(s.rb + cap); // c at the cursor (kEmpty: row done)
+    s.rwin = s.nextc + cap;                        // window of b's last recorded run
+    s.plen = s.rwin + cap;                         // length of b's last run (search hint)
+    return s;
+}
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 11ull * cap + 8; }
+
+
+// W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
+// or an open-addressing hash over all c < a (mid tops, HASH).  Hash keys are
+// u32 (kEmpty = free), counts u16 packed two per word.
+// cycle block kernel kinds: 0 dense windows (big tops), 1 block hash with
+// 2^15 slots (mid tops), 2 block hash with 2^13 slots and four 256-thread
+// blocks per SM (small-mid tops: their fixed per-top latency overlaps)
+template <int KIND> struct Cyc;
+template <> struct Cyc<0> {
+    static constexpr bool HASH = false;
+    static constexpr int THREADS = kBigThreads, MINB = kBigBlocksPerSM;
+    static constexpr u32 LOG = 0, WORDS = kWindow, META = 7168;
+};
+template <> struct Cyc<1> {
+    static constexpr bool HASH = true;
+    static constexpr int THREADS = kMidThreads, MINB = 1;
+    static constexpr u32 LOG = kMidLog, WORDS = (1u << kMidLog) * 3 / 2, META = 2048;
+};
+template <> struct Cyc<2> {
+    static constexpr bool HASH = true;
+    static constexpr int THREADS = kSmidThreads, MINB = 4;
+    static constexpr u32 LOG = kSmidLog, WORDS = (1u << kSmidLog) * 3 / 2, META = 256;
+};
+template <int KIND> __host__ __device__ constexpr u32 cyc_smem_words() {
+    return Cyc<KIND>::WORDS + 3 * Cyc<KIND>::META + 1;
+}
+
+
+template <int KIND>
+__device__ __forceinline__ void tab_inc(u32* W, u32 c, u32 lo, u32 cl) {
+    constexpr u32 NS = 1u << Cyc<KIND>::LOG;
+    if (Cyc<KIND>::HASH) {
+        u32* keys = W;
+        u32 h = (c * 0x9E3779B1u) >> ((32 - Cyc<KIND>::LOG) & 31);
+        for (;;) {
+            const u32 k = keys[h];
+            if (k == c) break;
+            if (k == kEmpty) {
+                const u32 prev = atomicCAS(&keys[h], kEmpty, c);
+                if (prev == kEmpty || prev == c) break;
+            }
+            h = (h + 1) & (NS - 1);
+        }
+        atomicAdd(&W[NS + (h >> 1)], 1u << ((h & 1) << 4));
+    } else {
+        w_inc(W, c - lo, cl);
+    }
+}
+template <int KIND>
+__device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, u32 cl) {
+    constexpr u32 NS = 1u << Cyc<KIND>::LOG;
+    if (Cyc<KIND>::HASH) {
+        u32 h = (c * 0x9E3779B1u) >> ((32 - Cyc<KIND>::LOG) & 31);
+        while (W[h] != c) h = (h + 1) & (NS - 1);
+        return (W[NS + (h >> 1)] >> ((h & 1) << 4)) & 0xffffu;
+    } else {
+        return w_get(W, c - lo, cl);
+    }
+}
+// dense windows only: the hash is always bulk-cleared (a deleted key would
+// break the probe chains of the clears still to come)
+__device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, u32 cl) { W[(c - lo) >> cl] = 0; }
+
+template <int KIND, int PASS>
+__device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, u32 cl, i64* __restrict__ slot_acc, u64 slot,
+                                         u64& val) {
+    if (!Cyc<KIND>::HASH) { // dense window: 32-bit shared addresses, predicated RED
+        const u32 ci = cv - lo;
+        const u32 addr = smem_u32(W) + ((ci >> cl) << 2);
+        const u32 sh = (ci & ((1u << cl) - 1u)) << (5 - cl);
+        if (PASS == 0) {
+            red_shared_add(addr, 1u << sh);
+        } else if (PASS == 1) {
+            const u32 w = ld_shared(addr) >> sh;
+            const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
+            red_add_u64_if(&slot_acc[slot], (u64)v);
+            val = v;
+        } else {
+            W[ci >> cl] = 0;
+        }
+        return;
+    }
+    if (PASS == 0) {
+        tab_inc<KIND>(W, cv, lo, cl);
+    } else if (PASS == 1) {
+        const u32 v = tab_get<KIND>(W, cv, lo, cl) - 1u;
+        if (v) atomic_add_i64(&slot_acc[slot], (i64)v);
+        val = v;
+    } else {
+        tab_clear_one(W, cv, lo, cl);
+    }
+}
+
+// Last index in [0, n) with a[idx] <= x (a non-decreasing, a[0] <= x), by the
+// whole warp: 32 probes per step, so log32(n) dependent loads instead of log2(n).
+__device__ __forceinline__ u32 warp_upper_bound(const u32* a, u32 n, u32 x) {
+    const u32 lane = lane_id();
+    u32 lo = 0, hi = n;
+    while (hi - lo > 32u) {
+        const u32 step = (hi - lo + 31u) >> 5;
+        const u32 idx = lo + lane * step;
+        const bool ok = idx < hi && a[idx] <= x;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        lo += (31u - __clz(bal)) * step;
+        hi = lo + step < hi ? lo + step : hi;
+    }
+    const u32 idx = lo + lane;
+    const unsigned bal = __ballot_sync(0xffffffffu, idx < hi && a[idx] <= x);
+    return lo + 31u - __clz(bal);
+}
+
+// One pass over a warp's range [kb, ke) of a window's flattened wedge list
+// (compacted runs q, S.pre = wedge prefix, run q = adjacency slots
+// [S.rs[q], S.rs[q] + len)).  Stretches of full 32-wedge rounds inside one
+// run take the uniform path: slot = base + lane, four rounds of loads in
+// flight, the (a,b) credit kept per lane and warp-reduced once per stretch.
+// Rounds that straddle runs take the mixed path: each lane finds its run
+// among the next 32 starts by a 5-step shuffle search and the (a,b) credit is
+// a segmented shuffle sum whose tail lanes issue the RED.
+//   PASS 0: W[c]++     PASS 1: credit W[c]-1 to (b,c) and, summed, to (a,b)
+//   PASS 2: W[c] = 0 (sparse clear of a dense window)
+constexpr int kUnroll = 8; // uniform-path rounds with loads in flight per lane
+
+template <int KIND, int PASS>
+__device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,
+                                            u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
+    const u32 lane = lane_id();
+    if (kb >= ke) return;
+    u32 bs = warp_upper_bound(S.pre, nnz + 1, kb);
+    u32 k0 = kb;
+    while (k0 < ke) {
+        u32 e1 = S.pre[bs + 1];
+        while (e1 <= k0) e1 = S.pre[++bs + 1];
+        const u32 stop = e1 < ke ? e1 : ke;
+        if (stop - k0 >= 32u) {
+            // uniform stretch of full rounds inside run bs
+            const u32 nfull = (stop - k0) >> 5;
+#ifdef GL_CYCLE_PROF_ROUNDS
+            if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[12], (unsigned long long)nfull);
+#endif
+            const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
+            u64 acc = 0;
+            // software pipeline: the next kHalf rounds' loads are in flight
+            // while the current kHalf rounds update the window
+            constexpr int kHalf = kUnroll / 2;
+            u32 cv[kHalf];
+#pragma unroll
+            for (int u = 0; u < kHalf; ++u) cv[u] = (u32)u < nfull ? __ldg(g.adj + sbase + 32u * u) : kEmpty;
+            for (u32 r = 0; r < nfull; r += kHalf) {
+                u32 nx[kHalf];
+#pragma unroll
+                for (int u = 0; u < kHalf; ++u)
+                    nx[u] = r + kHalf + u < nfull ? __ldg(g.adj + sbase + 32u * (r + kHalf + u)) : kEmpty;
+#pragma unroll
+                for (int u = 0; u < kHalf; ++u) {
+                    if (cv[u] != kEmpty) {
+                        u64 v = 0;
+                        wedge_op<KIND, PASS>(W, cv[u], lo, cl, slot_acc, sbase + 32u * (r + u), v);
+                        acc += v;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kHalf; ++u) cv[u] = nx[u];
+            }
+            if (PASS == 1) {
+                acc = warp_sum_u64(acc);
+                if (lane == 0 && acc) atomic_add_i64(&slot_acc[abase + S.rj[bs]], (i64)acc);
+            }
+            k0 += nfull << 5;
+        } else {
+            // mixed round [k0, k0 + 32): runs bs, bs+1, ... start at pre[bs+j];
+            // one OR-reduction gives the bitmask of run starts inside the round,
+            // from which every lane reads its run (popcount), its offset and
+            // its segment (highest start at or below it)
+#ifdef GL_CYCLE_PROF_ROUNDS
+            if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[13], 1ull);
+#endif
+            const u32 k = k0 + lane;
+            const bool valid = k < ke;
+            const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
+            const u32 rel = pi - k0; // >= 1 for lanes >= 1 (pre strictly increasing)
+            const u32 starts = __reduce_or_sync(0xffffffffu, (lane > 0 && rel < 32u) ? 1u << rel : 0u);
+            const u32 le = starts & (0xffffffffu >> (31 - lane)); // starts at or below this lane
+            const u32 owner = __popc(le);
+            const u32 q = bs + owner;
+            const u32 seg0 = owner ? 31u - __clz(le) : 0u;
+            const u32 pi0 = __shfl_sync(0xffffffffu, pi, 0); // all lanes: full-mask shuffle
+            const u32 off = owner ? lane - seg0 : k - pi0;
+            u64 v = 0;
+            if (valid) {
+                const u64 slot = (u64)S.rs[q] + off;
+                wedge_op<KIND, PASS>(W, __ldg(g.adj + slot), lo, cl, slot_acc, slot, v);
+            }
+            if (PASS == 1) {
+                const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));
+                if (cl) {
+                    // counters of <= 16 bits: the segment sum fits u32
+                    u32 v32 = (u32)v;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const u32 t = __shfl_up_sync(0xffffffffu, v32, d);
+                        if (lane >= seg0 + (u32)d) v32 += t;
+                    }
+                    if (tail && v32) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v32);
+                } else {
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const u64 t = __shfl_up_sync(0xffffffffu, v, d);
+                        if (lane >= seg0 + (u32)d) v += t;
+                    }
+                    if (tail && v) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v);
+                }
+            }
+            k0 += 32;
+            bs = __shfl_sync(0xffffffffu, q, 31);
+        }
+    }
+}
+
+// Guided self-scheduling of a window pass: a warp grabs about 1/(2*nwarps) of
+// the wedges still unclaimed (at most 8192, at least 64), so the grabs shrink
+// towards the end of the pass and the block's barrier waits for a short tail.
+__device__ __forceinline__ u32 grab_size(u32 remaining, u32 nwarps) {
+    u32 g = remaining / (2u * nwarps);
+    g = g < 8192u ? g : 8192u;
+    g = (g + 31u) & ~31u;
+    return g > 64u ? g : 64u;
+}
+
+// Mid and big tops: one block per top a (persistent blocks, atomic queue over
+// the cost-sorted list).  Big tops (!HASH) sweep c in dense shared-memory
+// windows (16-bit packed counters while |L(a)| < 65536: 2*kWindow c-values
+// per window, else 32-bit: kWindow); per window the non-empty runs
+// N(b) n [lo,hi) of the lower neighbours b are found by galloping from each
+// b's cursor, compacted (flag scan) and prefix-summed -- in shared memory when
+// they fit (RunMeta) -- and walked by window_pass, warps grabbing kGrab-wedge
+// ranges from a shared counter so that the cost differences between long-run
+// and short-run ranges do not stall the block at the pass barriers.  Mid tops
+// (HASH, <= kMidWedges wedges) take all c < a at once in a block hash: runs
+// are the full row prefixes N(b) n [0,a), one "window", no cursors.  Credits
+// go to per-adjacency-slot accumulators (consecutive wedges of a run are
+// consecutive slots), folded into edge rows by k_fold_slots.
+template <int KIND, int PASS>
+__device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u32 nnz, u32 T, u32* counter, u32* W,
+                                          u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
+    const u32 nwarps = blockDim.x >> 5;
+    for (;;) {
+        u32 k0 = 0, grab = 0;
+        if (lane_id() == 0) {
+            const u32 seen = *(volatile u32*)counter;
+            grab = grab_size(seen < T ? T - seen : 0u, nwarps);
+            k0 = atomicAdd(counter, grab);
+        }
+        k0 = __shfl_sync(0xffffffffu, k0, 0);
+        grab = __shfl_sync(0xffffffffu, grab, 0);
+        if (k0 >= T) break;
+        window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, cl, abase, slot_acc);
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
+k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
+              i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap, uint4 tiers) {
+    constexpr bool HASH = Cyc<KIND>::HASH;
+    constexpr int THREADS = Cyc<KIND>::THREADS;
+    constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
+    extern __shared__ u32 W[]; // kWords table words, then the run metadata
+    __shared__ unsigned long long s_idx;
+    __shared__ u32 s_next, s_work[3];
+    BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
+    const RunMeta Msm{W + kWords, W + kWords + kMeta + 1, W + kWords + 2 * kMeta + 1};
+    const RunMeta Mgl{S.pre, S.rs, S.rj};
+    for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
+#ifdef GL_CYCLE_PROF
+    // make prof: per-phase clock64 totals (thread 0, between barriers): 0 setup,
+    // 6 gallop, 1 scan, 2 compaction, 3 pass 0, 4 pass 1, 7 clear, 5 grab;
+    // 8 windows, 9 wedges, 10 tops (scripts/cycle_phases.py)
+    unsigned long long pf[11] = {0};
+    unsigned long long pt = clock64();
+#define GL_PROF_MARK(k)                                   \
+    if (threadIdx.x == 0) {                               \
+        const unsigned long long now_ = clock64();        \
+        pf[k] += now_ - pt;                               \
+        pt = now_;                                        \
+    }
+#define GL_PROF_SYNC_MARK(k) \
+    __syncthreads();         \
+    GL_PROF_MARK(k)
+#define GL_PROF_ADD(k, v) \
+    if (threadIdx.x == 0) pf[k] += (v);
+#else
+#define GL_PROF_MARK(k)
+#define GL_PROF_SYNC_MARK(k)
+#define GL_PROF_ADD(k, v)
+#endif
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_idx = atomicAdd(queue, 1ull);
+        __syncthreads();
+        const unsigned long long idx = s_idx;
+        if (idx >= n_items) break;
+        GL_PROF_MARK(5);
+        const u32 a = items[idx];
+        const u64 E0 = g.loff[a];
+        const u32 nb = (u32)(g.loff[a + 1] - E0);
+        const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
+
+        if (threadIdx.x == 0) s_next = HASH ? 0u : kEmpty;
+        __syncthreads();
+        // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at 0
+        for (u32 j = threadIdx.x; j < nb; j += THREADS) {
+            const u64 e = E0 + j;
+            const u64 rb = g.off[g.eu[e]];
+            const u32 re = g.epos[e];
+            S.rb[j] = rb;
+            S.rend[j] = re;
+            S.cur[j] = 0;
+            const u32 c = re > 0 ? g.adj[rb] : kEmpty;
+            S.nextc[j] = c;
+            S.rwin[j] = kEmpty;
+            S.plen[j] = 0;
+            if (!HASH && c != kEmpty) atomicMin(&s_next, c);
+        }
+        __syncthreads();
+        GL_PROF_MARK(0);
+        GL_PROF_ADD(10, 1);
+        // Windows from the smallest c on.  Each b keeps its cursor and the c
+        // value under it (nextc), so a window only gallops the b's whose next c
+        // falls inside it; for the others one coalesced nextc load suffices.
+        u32 win = 0;
+        for (u32 lo = s_next, hi = 0; lo < a; lo = hi, ++win) {
+            // window [lo, hi): inside one degree tier, counters of that tier's width
+            u32 cl = 1, tend = a;
+            if (!HASH) {
+                cl = lo < tiers.x ? 4u : lo < tiers.y ? 3u : lo < tiers.z ? 2u : lo < tiers.w ? 1u : 0u;
+                tend = lo < tiers.x ? tiers.x : lo < tiers.y ? tiers.y : lo < tiers.z ? tiers.z : lo < tiers.w ? tiers.w : a;
+            }
+            u64 span = (u64)kWindow << cl;
+            // keep nb * span < 2^31: window wedge counts and indices are u32
+            if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
+            hi = HASH ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)a);
+
+            // run ends of the b's with a c in [lo, hi); runs are ordered
+            // thread-major (thread t owns b = t + i*THREADS), so one block scan
+            // of per-thread (runs, wedges) places them
+            u32 my_runs = 0, my_wedges = 0;
+            for (u32 j0 = threadIdx.x; j0 < nb; j0 += kNcBatch * THREADS) {
+                u32 nc[kNcBatch];
+#pragma unroll
+                for (int u = 0; u < kNcBatch; ++u) {
+                    const u32 j = j0 + u * THREADS;
+                    nc[u] = j < nb ? S.nextc[j] : kEmpty;
+                }
+#pragma unroll
+                for (int u = 0; u < kNcBatch; ++u) {
+                    if (nc[u] >= hi) continue; // no c of b in this window (kEmpty >= hi)
+                    const u32 j = j0 + u * THREADS;
+                    const u32 c0 = S.cur[j], re = S.rend[j];
+                    const u64 rb = S.rb[j];
+                    u32 h = re;
+                    if (!HASH) {
+                        const u32 pl = S.plen[j];
+                        h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
+                        S.plen[j] = h - c0;
+                    }
+                    S.hpos[j] = c0; // run start
+                    S.rwin[j] = win;
+                    S.cur[j] = h;
+                    S.nextc[j] = h < re ? g.adj[rb + h] : kEmpty;
+                    ++my_runs;
+                    my_wedges += h - c0;
+                }
+            }
+            GL_PROF_SYNC_MARK(6);
+            u64 tot;
+            u64 mine = ((u64)my_runs << 32) | my_wedges;
+            {
+                using BlockScan = cub::BlockScan<u64, THREADS>;
+                __shared__ typename BlockScan::TempStorage tmp;
+                BlockScan(tmp).ExclusiveSum(mine, mine, tot);
+            }
+            const u32 nnz = (u32)(tot >> 32), T = (u32)tot;
+            GL_PROF_MARK(1);
+            GL_PROF_ADD(8, 1);
+            GL_PROF_ADD(9, T);
+            const RunMeta M = nnz <= kMeta ? Msm : Mgl;
+            if (my_runs) {
+                u32 q = (u32)(mine >> 32), w = (u32)mine;
+                for (u32 j0 = threadIdx.x; j0 < nb && q < (u32)(mine >> 32) + my_runs; j0 += kNcBatch * THREADS) {
+                    u32 rw[kNcBatch];
+#pragma unroll
+                    for (int u = 0; u < kNcBatch; ++u) {
+                        const u32 j = j0 + u * THREADS;
+                        rw[u] = j < nb ? S.rwin[j] : kEmpty;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kNcBatch; ++u) {
+                        if (rw[u] != win) continue;
+                        const u32 j = j0 + u * THREADS;
+                        const u32 c0 = S.hpos[j], h = S.cur[j];
+                        M.rj[q] = j;
+                        M.rs[q] = (u32)(S.rb[j] + c0);
+                        M.pre[q] = w;
+                        ++q;
+                        w += h - c0;
+                    }
+                }
+            }
+            if (threadIdx.x == 0) M.pre[nnz] = T;
+            if (threadIdx.x < 3) s_work[threadIdx.x] = 0;
+            __syncthreads();
+            GL_PROF_MARK(2);
+            if (T) {
+                const bool bulk_clear = HASH || T > kWords / 8;
+                {
+                    if (nnz <= kMeta) // shared-memory metadata: LDS in the walk
+                        grab_pass<KIND, 0>(g, Msm, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
+                    else
+                        grab_pass<KIND, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
+                }
+                __syncthreads();
+                GL_PROF_MARK(3);
+                {
+                    if (nnz <= kMeta)
+                        grab_pass<KIND, 1>(g, Msm, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
+                    else
+                        grab_pass<KIND, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
+                }
+                __syncthreads();
+                GL_PROF_MARK(4);
+                if (bulk_clear) {
+                    const u32 words = HASH ? kWords : (hi - lo + (1u << cl) - 1u) >> cl;
+                    for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
+                } else if (!HASH) {
+                    if (nnz <= kMeta)
+                        grab_pass<KIND, 2>(g, Msm, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
+                    else
+                        grab_pass<KIND, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
+                }
+            }
+            GL_PROF_SYNC_MARK(7);
+            __syncthreads();
+            GL_PROF_MARK(5);
+        }
+    }
+#ifdef GL_CYCLE_PROF
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 11; ++k) atomicAdd(&g_cycle_prof[k + (KIND ? 16 : 0)], pf[k]);
+#endif
+}
+
+// y(e) += the two adjacency-slot accumulators of edge e (v's row, u's row).
+__global__ void k_fold_slots(DevGraph g, const i64* __restrict__ slot_acc, i64* __restrict__ part) {
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < g.m; e += (u64)gridDim.x * blockDim.x) {
+        const u32 v = g.ev[e], u = g.eu[e];
+        const i64 s = slot_acc[g.off[v] + (e - g.loff[v])] + slot_acc[g.off[u] + g.epos[e]];
+        if (s) part[2 * e + 1] += s;
+    }
+}
+

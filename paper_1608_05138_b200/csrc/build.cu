@@ -4,11 +4,12 @@
 // Every step is a sort, a scan or a bandwidth-bound elementwise pass:
 //   1. label universe: radix-sort all 2*count endpoint labels, unique -> n
 //      (self-loop endpoints stay vertices, as in the reference)
-//   2. compact + canonicalise (min,max) into one u64 key, drop loops, radix
+//   2. compact + canonicalise (min,max) into one u64 key (min<<vb | max, vb =
+//      bits of the largest compact id, so 2*vb radix bits), drop loops, radix
 //      sort, unique -> m simple undirected edges
 //   3. degrees; P1 relabel by (degree asc, label asc) = radix sort of
-//      (deg<<32 | compact id) -- compact ids are already label-ordered
-//   4. both directions of every edge as (src<<32 | dst) keys, radix sort ->
+//      (deg<<vb | compact id) -- compact ids are already label-ordered
+//   4. both directions of every edge as (src<<vb | dst) keys, radix sort ->
 //      id-sorted rows (the reference's neighbors_by_id view)
 //   5. lcnt/loff/eid/ev/eu/epos: the oriented edge id of each slot is its rank
 //      in the lower prefix of the high endpoint's row, exactly the
@@ -87,7 +88,7 @@ __global__ void k_max_label(const u64* __restrict__ p, u64 n, unsigned long long
 
 // compact both endpoints by binary search in the unique label array
 __global__ void k_edge_keys(const u64* __restrict__ pairs, u64 count, const u64* __restrict__ labels,
-                            u64 n, u64 sentinel, u64* __restrict__ keys) {
+                            u64 n, u64 sentinel, int vb, u64* __restrict__ keys) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
         u64 a = pairs[2 * i], b = pairs[2 * i + 1];
         if (a == b) {
@@ -101,48 +102,52 @@ __global__ void k_edge_keys(const u64* __restrict__ pairs, u64 count, const u64*
             x = y;
             y = t;
         }
-        keys[i] = (x << 32) | y;
+        keys[i] = (x << vb) | y;
     }
 }
 
-__global__ void k_degree(const u64* __restrict__ keys, u64 m, u32* __restrict__ deg) {
+__global__ void k_degree(const u64* __restrict__ keys, u64 m, int vb, u32* __restrict__ deg) {
+    const u64 mask = ((u64)1 << vb) - 1;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
         u64 k = keys[i];
-        atomicAdd(&deg[k >> 32], 1u);
-        atomicAdd(&deg[k & 0xffffffffu], 1u);
+        atomicAdd(&deg[k >> vb], 1u);
+        atomicAdd(&deg[k & mask], 1u);
     }
 }
 
-__global__ void k_order_keys(const u32* __restrict__ deg, u64 n, u64* __restrict__ ok) {
+__global__ void k_order_keys(const u32* __restrict__ deg, u64 n, int vb, u64* __restrict__ ok) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
-        ok[i] = ((u64)deg[i] << 32) | i;
+        ok[i] = ((u64)deg[i] << vb) | i;
 }
 
 __global__ void k_relabel(const u64* __restrict__ sorted_ok, u64 n, const u64* __restrict__ labels,
                           u32* __restrict__ new_id, u32* __restrict__ deg_new,
-                          u64* __restrict__ label_new) {
+                          int vb, u64* __restrict__ label_new) {
+    const u64 mask = ((u64)1 << vb) - 1;
     for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < n; r += (u64)gridDim.x * blockDim.x) {
         u64 k = sorted_ok[r];
-        u32 old = (u32)(k & 0xffffffffu);
+        u32 old = (u32)(k & mask);
         new_id[old] = (u32)r;
-        deg_new[r] = (u32)(k >> 32);
+        deg_new[r] = (u32)(k >> vb);
         label_new[r] = labels[old];
     }
 }
 
 __global__ void k_directed(const u64* __restrict__ keys, u64 m, const u32* __restrict__ new_id,
-                           u64* __restrict__ dir) {
+                           int vb, u64* __restrict__ dir) {
+    const u64 mask = ((u64)1 << vb) - 1;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
         u64 k = keys[i];
-        u64 a = new_id[k >> 32], b = new_id[k & 0xffffffffu];
-        dir[2 * i] = (a << 32) | b;
-        dir[2 * i + 1] = (b << 32) | a;
+        u64 a = new_id[k >> vb], b = new_id[k & mask];
+        dir[2 * i] = (a << vb) | b;
+        dir[2 * i + 1] = (b << vb) | a;
     }
 }
 
-__global__ void k_adj_from_dir(const u64* __restrict__ dir, u64 len, u32* __restrict__ adj) {
+__global__ void k_adj_from_dir(const u64* __restrict__ dir, u64 len, int vb, u32* __restrict__ adj) {
+    const u64 mask = ((u64)1 << vb) - 1;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < len; i += (u64)gridDim.x * blockDim.x)
-        adj[i] = (u32)(dir[i] & 0xffffffffu);
+        adj[i] = (u32)(dir[i] & mask);
 }
 
 __global__ void k_widen(const u32* __restrict__ a, u64 n, u64* __restrict__ b) {
@@ -160,12 +165,12 @@ __global__ void k_lcnt(const u64* __restrict__ off, const u32* __restrict__ adj,
     }
 }
 
-__global__ void k_slots(const u64* __restrict__ dir, u64 len, const u64* __restrict__ off,
+__global__ void k_slots(const u64* __restrict__ dir, u64 len, int vb, const u64* __restrict__ off,
                         const u32* __restrict__ adj, const u32* __restrict__ lcnt,
                         const u64* __restrict__ loff, u32* __restrict__ eid, u32* __restrict__ ev,
                         u32* __restrict__ eu, u32* __restrict__ epos) {
     for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < len; j += (u64)gridDim.x * blockDim.x) {
-        u32 v = (u32)(dir[j] >> 32);
+        u32 v = (u32)(dir[j] >> vb);
         u32 x = adj[j];
         u64 pos = j - off[v];
         if (x < v) {
@@ -233,13 +238,16 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         DevBuf keys_a, keys_b;
         keys_a.alloc((count + 1) * sizeof(u64));
         keys_b.alloc((count + 1) * sizeof(u64));
-        const u64 sentinel = ((((u64)1 << vb) - 1) << 32) | 0xffffffffull;
+        // keys pack (x << vb) | y into 2*vb bits so the radix sorts skip the
+        // always-zero gap a fixed 32-bit split would leave
+        const int kb = 2 * vb;
+        const u64 sentinel = kb >= 64 ? ~0ull : (((u64)1 << kb) - 1);
         u64 m = 0;
         if (count > 0) {
-            k_edge_keys<<<grid_for(count), kThreads, 0, s>>>(d_pairs, count, labels, n, sentinel,
+            k_edge_keys<<<grid_for(count), kThreads, 0, s>>>(d_pairs, count, labels, n, sentinel, vb,
                                                                keys_a.as<u64>());
             GL_LAUNCH_CHECK();
-            sort_keys<u64>(tmp, keys_a.as<u64>(), keys_b.as<u64>(), count, 32 + vb, s);
+            sort_keys<u64>(tmp, keys_a.as<u64>(), keys_b.as<u64>(), count, kb, s);
             u64 nu = unique_keys<u64>(tmp, keys_b.as<u64>(), keys_a.as<u64>(), count, cnt, s);
             u64 last = 0;
             if (nu > 0) {
@@ -258,7 +266,7 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         deg_old.alloc((n + 1) * sizeof(u32));
         GL_CUDA(cudaMemsetAsync(deg_old.p, 0, (n + 1) * sizeof(u32), s));
         if (m) {
-            k_degree<<<grid_for(m), kThreads, 0, s>>>(ekeys, m, deg_old.as<u32>());
+            k_degree<<<grid_for(m), kThreads, 0, s>>>(ekeys, m, vb, deg_old.as<u32>());
             GL_LAUNCH_CHECK();
         }
         g->b_deg.alloc((n + 1) * sizeof(u32));
@@ -273,11 +281,11 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
             GL_CUDA(cudaStreamSynchronize(s));
             okeys_a.alloc(n * sizeof(u64));
             okeys_b.alloc(n * sizeof(u64));
-            k_order_keys<<<grid_for(n), kThreads, 0, s>>>(deg_old.as<u32>(), n, okeys_a.as<u64>());
+            k_order_keys<<<grid_for(n), kThreads, 0, s>>>(deg_old.as<u32>(), n, vb, okeys_a.as<u64>());
             GL_LAUNCH_CHECK();
-            sort_keys<u64>(tmp, okeys_a.as<u64>(), okeys_b.as<u64>(), n, 32 + bits_for(dmax), s);
+            sort_keys<u64>(tmp, okeys_a.as<u64>(), okeys_b.as<u64>(), n, vb + bits_for(dmax), s);
             k_relabel<<<grid_for(n), kThreads, 0, s>>>(okeys_b.as<u64>(), n, labels, new_id.as<u32>(),
-                                                       g->b_deg.as<u32>(), g->b_label.as<u64>());
+                                                       g->b_deg.as<u32>(), vb, g->b_label.as<u64>());
             GL_LAUNCH_CHECK();
         }
         okeys_a.reset();
@@ -301,12 +309,12 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         if (m) {
             dir_a.alloc(len * sizeof(u64));
             dir_b.alloc(len * sizeof(u64));
-            k_directed<<<grid_for(m), kThreads, 0, s>>>(ekeys, m, new_id.as<u32>(), dir_a.as<u64>());
+            k_directed<<<grid_for(m), kThreads, 0, s>>>(ekeys, m, new_id.as<u32>(), vb, dir_a.as<u64>());
             GL_LAUNCH_CHECK();
             keys_a.reset();
-            sort_keys<u64>(tmp, dir_a.as<u64>(), dir_b.as<u64>(), len, 32 + vb, s);
+            sort_keys<u64>(tmp, dir_a.as<u64>(), dir_b.as<u64>(), len, kb, s);
             dir_a.reset();
-            k_adj_from_dir<<<grid_for(len), kThreads, 0, s>>>(dir_b.as<u64>(), len, g->b_adj.as<u32>());
+            k_adj_from_dir<<<grid_for(len), kThreads, 0, s>>>(dir_b.as<u64>(), len, vb, g->b_adj.as<u32>());
             GL_LAUNCH_CHECK();
         }
         new_id.reset();
@@ -327,7 +335,7 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
             exclusive_scan<u64>(tmp, tmp64.as<u64>(), g->b_loff.as<u64>(), n + 1, s);
         }
         if (m) {
-            k_slots<<<grid_for(len), kThreads, 0, s>>>(dir_b.as<u64>(), len, g->b_off.as<u64>(),
+            k_slots<<<grid_for(len), kThreads, 0, s>>>(dir_b.as<u64>(), len, vb, g->b_off.as<u64>(),
                                                        g->b_adj.as<u32>(), g->b_lcnt.as<u32>(),
                                                        g->b_loff.as<u64>(), g->b_eid.as<u32>(),
                                                        g->b_ev.as<u32>(), g->b_eu.as<u32>(),

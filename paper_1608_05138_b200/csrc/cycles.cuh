@@ -444,6 +444,37 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
     }
 }
 
+// One pass over a window's runs.  Run metadata that did not fit in shared
+// memory (nnz > kMeta, written to the block's global scratch by the
+// compaction) is staged back through shared memory kMeta runs at a time, so
+// the walk's run lookups stay LDS instead of dependent L2 round trips; the
+// W window is complete before the pass starts, so chunking changes nothing.
+template <int KIND, int PASS>
+__device__ __forceinline__ void meta_pass(const DevGraph& g, const RunMeta& Msm, const RunMeta& Mgl, u32 nnz, u32 T,
+                                          u32* counter, u32* W, u32 lo, u32 cl, u64 abase,
+                                          i64* __restrict__ slot_acc) {
+    constexpr u32 kMeta = Cyc<KIND>::META;
+    if (nnz <= kMeta) {
+        grab_pass<KIND, PASS>(g, Msm, nnz, T, counter, W, lo, cl, abase, slot_acc);
+        return;
+    }
+    for (u32 q0 = 0; q0 < nnz; q0 += kMeta) {
+        const u32 nq = nnz - q0 < kMeta ? nnz - q0 : kMeta;
+        const u32 base = Mgl.pre[q0], end = Mgl.pre[q0 + nq];
+        __syncthreads(); // the previous chunk's walkers are done with Msm
+        for (u32 i = threadIdx.x; i <= nq; i += blockDim.x) {
+            Msm.pre[i] = Mgl.pre[q0 + i] - base;
+            if (i < nq) {
+                Msm.rs[i] = Mgl.rs[q0 + i];
+                Msm.rj[i] = Mgl.rj[q0 + i];
+            }
+        }
+        if (threadIdx.x == 0) *counter = 0;
+        __syncthreads();
+        grab_pass<KIND, PASS>(g, Msm, nq, end - base, counter, W, lo, cl, abase, slot_acc);
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
@@ -570,6 +601,15 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             GL_PROF_MARK(1);
             GL_PROF_ADD(8, 1);
             GL_PROF_ADD(9, T);
+#ifdef GL_CYCLE_PROF
+            if (KIND == 0 && threadIdx.x == 0) {
+                atomicAdd(&g_cycle_prof[11], (unsigned long long)nnz);
+                if (nnz > kMeta) {
+                    atomicAdd(&g_cycle_prof[14], 1ull);
+                    atomicAdd(&g_cycle_prof[15], (unsigned long long)T);
+                }
+            }
+#endif
             const RunMeta M = nnz <= kMeta ? Msm : Mgl;
             if (my_runs) {
                 u32 q = (u32)(mine >> 32), w = (u32)mine;
@@ -600,18 +640,12 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             if (T) {
                 const bool bulk_clear = HASH || T > kWords / 8;
                 {
-                    if (nnz <= kMeta) // shared-memory metadata: LDS in the walk
-                        grab_pass<KIND, 0>(g, Msm, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
-                    else
-                        grab_pass<KIND, 0>(g, Mgl, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
+                    meta_pass<KIND, 0>(g, Msm, Mgl, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
                 }
                 __syncthreads();
                 GL_PROF_MARK(3);
                 {
-                    if (nnz <= kMeta)
-                        grab_pass<KIND, 1>(g, Msm, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
-                    else
-                        grab_pass<KIND, 1>(g, Mgl, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
+                    meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
                 }
                 __syncthreads();
                 GL_PROF_MARK(4);
@@ -619,10 +653,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                     const u32 words = HASH ? kWords : (hi - lo + (1u << cl) - 1u) >> cl;
                     for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
                 } else if (!HASH) {
-                    if (nnz <= kMeta)
-                        grab_pass<KIND, 2>(g, Msm, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
-                    else
-                        grab_pass<KIND, 2>(g, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
+                    meta_pass<KIND, 2>(g, Msm, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
                 }
             }
             GL_PROF_SYNC_MARK(7);

@@ -35,5 +35,6 @@ for base, kind in ((0, "dense windows"), (16, "mid hash")):
         print(f"  {nm:12s} {buf[base + i] / 1e6:10.1f} Mcyc  {100 * buf[base + i] / tot:5.1f}%")
     if base == 0:
         print(f"  pass-1 rounds: uniform {buf[12]}  mixed {buf[13]}")
+        print(f"  runs {buf[11]}  windows with global run metadata {buf[14]} ({buf[15]} wedges)")
     w, T, tops = buf[base + 8], buf[base + 9], buf[base + 10]
     print(f"  windows {w}  wedges {T}  tops {tops}  wedges/window {T / max(1, w):.0f}")

@@ -57,6 +57,11 @@ constexpr int kMidLog = 15;
 constexpr u32 kMidSlots = 1u << kMidLog; // mid tops: block hash, u32 keys + u16 counts (192 KB)
 constexpr u64 kMidWedges = kMidSlots / 2; // mid-top threshold (<= half the hash slots)
 constexpr int kSmidLog = 13;
+// sparse big tops (windowed block hash): c windows sized for ~kHashWinTarget
+// wedges, re-cut when a window holds more than kHashWinMax (and spans more
+// than kHashWinMax ids), so a window's distinct c ids stay <= 5/8 of the slots
+constexpr u32 kHashWinTarget = 12288;
+constexpr u32 kHashWinMax = 20480;
 constexpr u64 kSmidWedges = (1u << kSmidLog) / 2; // small-mid threshold
 
 constexpr u32 kEmpty = 0xffffffffu;
@@ -248,16 +253,47 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
     if (hb) atomicAdd(hedge_bound, hb);
 }
 
-// cycle work list key = wedges of top a; classes big (> kMidWedges, dense
-// windows), mid (> kSmallWedges, block hash), small (warp hash)
-__global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u32* __restrict__ keys,
-                           unsigned long long* __restrict__ n_big, unsigned long long* __restrict__ n_mid,
-                           unsigned long long* __restrict__ n_smid, unsigned long long* __restrict__ n_small) {
-    unsigned long long lb = 0, lm = 0, lq = 0, ls = 0;
+// dense windows a big top sweeps: the c range [0, a) cut at the degree tiers,
+// kWindow << cl ids per window of tier width cl
+__device__ __forceinline__ u64 dense_windows(u32 a, const unsigned* __restrict__ tiers) {
+    u64 nw = 0;
+    u32 prev = 0;
+    for (int i = 0; i <= 4; ++i) {
+        const u32 end = i < 4 ? (tiers[i] < a ? tiers[i] : a) : a;
+        const u64 span = (u64)kWindow << (4 - i);
+        if (end > prev) nw += (end - prev + span - 1) / span;
+        prev = end > prev ? end : prev;
+    }
+    return nw;
+}
+
+// Sparse big tops take the windowed hash when factor * (hash windows) <=
+// (dense windows).  GL_SPARSE_BIG=all|off overrides (tests force both paths).
+inline u32 sparse_big_factor() {
+    const char* e = std::getenv("GL_SPARSE_BIG");
+    if (e && !std::strcmp(e, "all")) return 0u;
+    if (e && !std::strcmp(e, "off")) return 0xffffffffu;
+    return 4u;
+}
+
+// cycle work list key = wedges of top a; classes sparse big (> kMidWedges,
+// wedges thin over the c range: windowed block hash), big (dense windows),
+// mid (> kSmallWedges, block hash), small (warp hash)
+__global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, const unsigned* __restrict__ tiers,
+                           u32* __restrict__ keys, unsigned long long* __restrict__ n_big,
+                           unsigned long long* __restrict__ n_mid, unsigned long long* __restrict__ n_smid,
+                           unsigned long long* __restrict__ n_small, unsigned long long* __restrict__ n_sparse,
+                           u32 sparse_factor) {
+    unsigned long long lb = 0, lm = 0, lq = 0, ls = 0, lh = 0;
     for (u64 a = blockIdx.x * (u64)blockDim.x + threadIdx.x; a < g.n; a += (u64)gridDim.x * blockDim.x) {
         u64 w = wpre[g.loff[a + 1]] - wpre[g.loff[a]];
         u32 cls = 0; // exact class boundaries: class above the log cost
-        if (w > kMidWedges) {
+        const u64 nb = g.loff[a + 1] - g.loff[a];
+        if (w > kMidWedges && nb < 65536 &&
+            (u64)sparse_factor * ((w + kHashWinTarget - 1) / kHashWinTarget) <= dense_windows((u32)a, tiers)) {
+            ++lh; // u16 hash counts: W <= nb < 65536
+            cls = 5;
+        } else if (w > kMidWedges) {
             ++lb;
             cls = 4;
         } else if (w > kSmidWedges) {
@@ -272,6 +308,7 @@ __global__ void k_top_keys(DevGraph g, const u64* __restrict__ wpre, u32* __rest
         }
         keys[a] = (cls << 12) | log_key(w);
     }
+    if (lh) atomicAdd(n_sparse, lh);
     if (lb) atomicAdd(n_big, lb);
     if (lm) atomicAdd(n_mid, lm);
     if (lq) atomicAdd(n_smid, lq);
@@ -301,7 +338,8 @@ __global__ void k_tiers(DevGraph g, unsigned* __restrict__ out) {
 // 1/2/4/7 cycle big/small/mid/small-mid queues, 3 H warp queue, 5/6/9/26 sums
 // large/warp/medium/xl queues, 8 H medium queue, 25 H xl queue, 10/11/15/16
 // cycle class counts, 12/13/21/24 H class counts (large/small/medium/xl),
-// 14 max k, 17 s1, 18 max s1, 19 H-edge bound, 20 H-edge list fill, 22-23 tiers
+// 14 max k, 17 s1, 18 max s1, 19 H-edge bound, 20 H-edge list fill, 22-23 tiers,
+// 27 sparse-big cycle class count, 28 its queue
 constexpr int kCounters = 32;
 
 // rank's share of a cost-sorted list: sorted positions p with p % world == rank
@@ -546,28 +584,35 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* kout = kin + (n + 1);
             u32* iin = cs.items_c.as<u32>();
             u32* iout = iin + (n + 1);
-            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), kin, counters + 10, counters + 15,
-                                                           counters + 16, counters + 11);
             k_tiers<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, (unsigned*)(counters + 22));
+            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), (const unsigned*)(counters + 22),
+                                                           kin, counters + 10, counters + 15, counters + 16,
+                                                           counters + 11, counters + 27, sparse_big_factor());
             k_seq<<<grid1d(n, 256, sms), 256, 0, s2>>>(iin, n);
             GL_LAUNCH_CHECK();
             dev_sort_desc(cs.tmp_c, kin, kout, iin, iout, n, s2);
             u64 cc[kCounters];
             GL_CUDA(cudaMemcpyAsync(cc, counters, sizeof(cc), cudaMemcpyDeviceToHost, s2));
             const u64 wtot = read_dev(cs.wpre.as<u64>() + m, s2);
-            const u64 nbig = cc[10], nmid = cc[15], nsmid = cc[16], nsmall = cc[11];
+            const u64 nsparse = cc[27], nbig = cc[10], nmid = cc[15], nsmid = cc[16], nsmall = cc[11];
+            if (std::getenv("GL_DEBUG"))
+                std::fprintf(stderr, "[gl] cycle classes sparse-big %llu big %llu mid %llu small-mid %llu small %llu\n",
+                             (unsigned long long)nsparse, (unsigned long long)nbig, (unsigned long long)nmid,
+                             (unsigned long long)nsmid, (unsigned long long)nsmall);
             const uint4 tiers = make_uint4((u32)cc[22], (u32)(cc[22] >> 32), (u32)cc[23], (u32)(cc[23] >> 32));
             cs.work[2] = 12 * wtot / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
+            const u64 mysparse = rank_share(nsparse, rank, world);
             const u64 mybig = rank_share(nbig, rank, world);
             const u64 mymid = rank_share(nmid, rank, world);
             const u64 mysmid = rank_share(nsmid, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
-            u32* lbig = iin;
+            u32* lsparse = iin;
+            u32* lbig = lsparse + mysparse;
             u32* lmid = lbig + mybig;
             u32* lsmid = lmid + mymid;
             u32* lsmall = lsmid + mysmid;
-            if (mybig || mymid || mysmid) {
+            if (mysparse || mybig || mymid || mysmid) {
                 if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
                 // per-block scratch: big tops need dmax + 2 entries, hash tops at most
                 // their wedge bound (nb <= wedges)
@@ -575,12 +620,12 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const u32 cap_hash = std::min<u32>(cap_big, (u32)kMidWedges + 2);
                 const u64 w_big = (big_scratch_words(cap_big) + 1) & ~1ull;
                 const u64 w_hash = (big_scratch_words(cap_hash) + 1) & ~1ull;
-                if (mybig) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
+                if (mybig || mysparse) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
                 if (mymid || mysmid) cs.cursor2.alloc((u64)sms * 4 * w_hash * sizeof(u32));
                 auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
                     constexpr int K = decltype(kind)::value;
-                    const u32 cap = K == 0 ? cap_big : cap_hash;
-                    u32* scratch = K == 0 ? cs.cursor.as<u32>() : cs.cursor2.as<u32>();
+                    const u32 cap = K == 0 || K == 3 ? cap_big : cap_hash;
+                    u32* scratch = K == 0 || K == 3 ? cs.cursor.as<u32>() : cs.cursor2.as<u32>();
                     k_take_rank<<<grid1d(count, 256, sms), 256, 0, s2>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
@@ -590,12 +635,16 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };
-                if (mybig) launch(std::integral_constant<int, 0>{}, lbig, mybig, 0, nbig, counters + 1);
-                if (mymid) launch(std::integral_constant<int, 1>{}, lmid, mymid, nbig, nmid, counters + 4);
-                if (mysmid) launch(std::integral_constant<int, 2>{}, lsmid, mysmid, nbig + nmid, nsmid, counters + 7);
+                // sorted list: [sparse big | big | mid | small-mid | small]
+                if (mysparse) launch(std::integral_constant<int, 3>{}, lsparse, mysparse, 0, nsparse, counters + 28);
+                if (mybig) launch(std::integral_constant<int, 0>{}, lbig, mybig, nsparse, nbig, counters + 1);
+                if (mymid) launch(std::integral_constant<int, 1>{}, lmid, mymid, nsparse + nbig, nmid, counters + 4);
+                if (mysmid)
+                    launch(std::integral_constant<int, 2>{}, lsmid, mysmid, nsparse + nbig + nmid, nsmid, counters + 7);
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s2>>>(iout, nbig + nmid + nsmid, nsmall, rank, world, lsmall);
+                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s2>>>(iout, nsparse + nbig + nmid + nsmid, nsmall, rank,
+                                                                       world, lsmall);
                 GL_LAUNCH_CHECK();
                 const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
                 smem_attr(k_cycle_small, smem, gr.device);

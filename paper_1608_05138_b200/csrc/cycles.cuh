@@ -190,22 +190,31 @@ __host__ __device__ inline u64 big_scratch_words(u32 cap) { return 11ull * cap +
 // u32 (kEmpty = free), counts u16 packed two per word.
 // cycle block kernel kinds: 0 dense windows (big tops), 1 block hash with
 // 2^15 slots (mid tops), 2 block hash with 2^13 slots and four 256-thread
-// blocks per SM (small-mid tops: their fixed per-top latency overlaps)
+// blocks per SM (small-mid tops: their fixed per-top latency overlaps),
+// 3 windowed block hash (sparse big tops: c windows cut by wedge count, not by
+// the shared-memory span, so a top whose wedges are thin over a wide c range
+// takes a few hash windows instead of many near-empty dense ones).  WIN: the
+// c range is swept in windows with per-b cursors.
 template <int KIND> struct Cyc;
 template <> struct Cyc<0> {
-    static constexpr bool HASH = false;
+    static constexpr bool HASH = false, WIN = true;
     static constexpr int THREADS = kBigThreads, MINB = kBigBlocksPerSM;
     static constexpr u32 LOG = 0, WORDS = kWindow, META = 7168;
 };
 template <> struct Cyc<1> {
-    static constexpr bool HASH = true;
+    static constexpr bool HASH = true, WIN = false;
     static constexpr int THREADS = kMidThreads, MINB = 1;
     static constexpr u32 LOG = kMidLog, WORDS = (1u << kMidLog) * 3 / 2, META = 2048;
 };
 template <> struct Cyc<2> {
-    static constexpr bool HASH = true;
+    static constexpr bool HASH = true, WIN = false;
     static constexpr int THREADS = kSmidThreads, MINB = 4;
     static constexpr u32 LOG = kSmidLog, WORDS = (1u << kSmidLog) * 3 / 2, META = 256;
+};
+template <> struct Cyc<3> {
+    static constexpr bool HASH = true, WIN = true;
+    static constexpr int THREADS = kMidThreads, MINB = 1;
+    static constexpr u32 LOG = kMidLog, WORDS = (1u << kMidLog) * 3 / 2, META = 2048;
 };
 template <int KIND> __host__ __device__ constexpr u32 cyc_smem_words() {
     return Cyc<KIND>::WORDS + 3 * Cyc<KIND>::META + 1;
@@ -479,11 +488,11 @@ template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap, uint4 tiers) {
-    constexpr bool HASH = Cyc<KIND>::HASH;
+    constexpr bool HASH = Cyc<KIND>::HASH, WIN = Cyc<KIND>::WIN;
     constexpr int THREADS = Cyc<KIND>::THREADS;
     constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
     extern __shared__ u32 W[]; // kWords table words, then the run metadata
-    __shared__ unsigned long long s_idx;
+    __shared__ unsigned long long s_idx, s_rem;
     __shared__ u32 s_next, s_work[3];
     BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
     const RunMeta Msm{W + kWords, W + kWords + kMeta + 1, W + kWords + 2 * kMeta + 1};
@@ -523,8 +532,12 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
 
-        if (threadIdx.x == 0) s_next = HASH ? 0u : kEmpty;
+        if (threadIdx.x == 0) {
+            s_next = WIN ? kEmpty : 0u;
+            s_rem = 0;
+        }
         __syncthreads();
+        u64 my_rem = 0;
         // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at 0
         for (u32 j = threadIdx.x; j < nb; j += THREADS) {
             const u64 e = E0 + j;
@@ -537,9 +550,12 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             S.nextc[j] = c;
             S.rwin[j] = kEmpty;
             S.plen[j] = 0;
-            if (!HASH && c != kEmpty) atomicMin(&s_next, c);
+            if (WIN && c != kEmpty) atomicMin(&s_next, c);
+            my_rem += re;
         }
+        if (KIND == 3 && my_rem) atomicAdd(&s_rem, (unsigned long long)my_rem);
         __syncthreads();
+        u64 rem = s_rem; // wedges of this top not yet in a window (KIND 3 window sizing)
         GL_PROF_MARK(0);
         GL_PROF_ADD(10, 1);
         // Windows from the smallest c on.  Each b keeps its cursor and the c
@@ -554,50 +570,82 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 tend = lo < tiers.x ? tiers.x : lo < tiers.y ? tiers.y : lo < tiers.z ? tiers.z : lo < tiers.w ? tiers.w : a;
             }
             u64 span = (u64)kWindow << cl;
+            if (KIND == 3) { // about kHashWinTarget wedges if they were uniform over [lo, a)
+                span = rem ? (u64)(a - lo) * kHashWinTarget / rem : (u64)(a - lo);
+                span = span ? span : 1;
+            }
             // keep nb * span < 2^31: window wedge counts and indices are u32
             if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
-            hi = HASH ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)a);
+            hi = !WIN ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)a);
 
-            // run ends of the b's with a c in [lo, hi); runs are ordered
-            // thread-major (thread t owns b = t + i*THREADS), so one block scan
-            // of per-thread (runs, wedges) places them
-            u32 my_runs = 0, my_wedges = 0;
-            for (u32 j0 = threadIdx.x; j0 < nb; j0 += kNcBatch * THREADS) {
-                u32 nc[kNcBatch];
+            u32 my_runs, my_wedges, nnz, T;
+            u64 mine;
+            for (;;) {
+                // run ends of the b's with a c in [lo, hi); runs are ordered
+                // thread-major (thread t owns b = t + i*THREADS), so one block scan
+                // of per-thread (runs, wedges) places them
+                my_runs = 0, my_wedges = 0;
+                for (u32 j0 = threadIdx.x; j0 < nb; j0 += kNcBatch * THREADS) {
+                    u32 nc[kNcBatch];
 #pragma unroll
-                for (int u = 0; u < kNcBatch; ++u) {
-                    const u32 j = j0 + u * THREADS;
-                    nc[u] = j < nb ? S.nextc[j] : kEmpty;
-                }
-#pragma unroll
-                for (int u = 0; u < kNcBatch; ++u) {
-                    if (nc[u] >= hi) continue; // no c of b in this window (kEmpty >= hi)
-                    const u32 j = j0 + u * THREADS;
-                    const u32 c0 = S.cur[j], re = S.rend[j];
-                    const u64 rb = S.rb[j];
-                    u32 h = re;
-                    if (!HASH) {
-                        const u32 pl = S.plen[j];
-                        h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
-                        S.plen[j] = h - c0;
+                    for (int u = 0; u < kNcBatch; ++u) {
+                        const u32 j = j0 + u * THREADS;
+                        nc[u] = j < nb ? S.nextc[j] : kEmpty;
                     }
-                    S.hpos[j] = c0; // run start
-                    S.rwin[j] = win;
-                    S.cur[j] = h;
-                    S.nextc[j] = h < re ? g.adj[rb + h] : kEmpty;
-                    ++my_runs;
-                    my_wedges += h - c0;
+#pragma unroll
+                    for (int u = 0; u < kNcBatch; ++u) {
+                        if (nc[u] >= hi) continue; // no c of b in this window (kEmpty >= hi)
+                        const u32 j = j0 + u * THREADS;
+                        const u32 c0 = S.cur[j], re = S.rend[j];
+                        const u64 rb = S.rb[j];
+                        u32 h = re;
+                        if (WIN) {
+                            const u32 pl = S.plen[j];
+                            h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
+                            S.plen[j] = h - c0;
+                        }
+                        S.hpos[j] = c0; // run start
+                        S.rwin[j] = win;
+                        S.cur[j] = h;
+                        S.nextc[j] = h < re ? g.adj[rb + h] : kEmpty;
+                        ++my_runs;
+                        my_wedges += h - c0;
+                    }
                 }
+                GL_PROF_SYNC_MARK(6);
+                u64 tot;
+                mine = ((u64)my_runs << 32) | my_wedges;
+                {
+                    using BlockScan = cub::BlockScan<u64, THREADS>;
+                    __shared__ typename BlockScan::TempStorage tmp;
+                    BlockScan(tmp).ExclusiveSum(mine, mine, tot);
+                }
+                nnz = (u32)(tot >> 32), T = (u32)tot;
+                // a KIND 3 window over its wedge cap: restore its b's cursors
+                // and re-cut it narrower (a window of <= kHashWinMax ids is
+                // always accepted: its distinct c ids fit the slots anyway)
+                if (!(KIND == 3 && T > kHashWinMax && hi - lo > kHashWinMax)) break;
+#ifdef GL_CYCLE_PROF
+                if (threadIdx.x == 0) atomicAdd(&g_cycle_prof[29], 1ull); // KIND 3 re-cuts
+#endif
+                for (u32 j = threadIdx.x; j < nb; j += THREADS) {
+                    if (S.rwin[j] != win) continue;
+                    const u32 c0 = S.hpos[j];
+                    S.cur[j] = c0;
+                    S.nextc[j] = g.adj[S.rb[j] + c0];
+                    S.rwin[j] = kEmpty;
+                }
+                __syncthreads(); // BlockScan storage reuse
+                u64 nspan = (u64)(hi - lo) * kHashWinTarget / T;
+                hi = lo + (u32)(nspan ? nspan : 1);
             }
-            GL_PROF_SYNC_MARK(6);
-            u64 tot;
-            u64 mine = ((u64)my_runs << 32) | my_wedges;
-            {
-                using BlockScan = cub::BlockScan<u64, THREADS>;
-                __shared__ typename BlockScan::TempStorage tmp;
-                BlockScan(tmp).ExclusiveSum(mine, mine, tot);
+            rem -= T;
+#ifdef GL_CYCLE_PROF
+            if (KIND == 3 && threadIdx.x == 0) {
+                atomicAdd(&g_cycle_prof[30], 1ull);
+                atomicAdd(&g_cycle_prof[31], (unsigned long long)T);
             }
-            const u32 nnz = (u32)(tot >> 32), T = (u32)tot;
+#endif
             GL_PROF_MARK(1);
             GL_PROF_ADD(8, 1);
             GL_PROF_ADD(9, T);

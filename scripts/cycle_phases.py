@@ -38,3 +38,4 @@ for base, kind in ((0, "dense windows"), (16, "mid hash")):
         print(f"  runs {buf[11]}  windows with global run metadata {buf[14]} ({buf[15]} wedges)")
     w, T, tops = buf[base + 8], buf[base + 9], buf[base + 10]
     print(f"  windows {w}  wedges {T}  tops {tops}  wedges/window {T / max(1, w):.0f}")
+print(f"windowed-hash (sparse big) windows {buf[30]}  wedges {buf[31]}  re-cuts {buf[29]}")

@@ -170,6 +170,56 @@ def test_multiwindow_half_counters(cuda_device):
     assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
 
 
+@pytest.mark.parametrize("mode", ["all", "off"])
+@pytest.mark.parametrize("n,k,seed", [(60000, 6, 3), (200000, 4, 11), (30000, 12, 5)])
+def test_sparse_big_windowed_hash(cuda_device, monkeypatch, mode, n, k, seed):
+    """GL_SPARSE_BIG=all routes every big top (> 16384 wedges, |L(a)| < 65536)
+    through the windowed block hash (KIND 3: c windows cut by wedge count and
+    re-cut when over the cap); =off keeps them on dense windows."""
+    monkeypatch.setenv("GL_SPARSE_BIG", mode)
+    pairs = gl.generate_ba(n, k, seed=seed)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
+def recut_graph(seed=1):
+    """Top A (degree 300) over 100 b's whose wedges crowd the low end of a wide
+    c range: 1100 ids of degree 20 (C1) adjacent to 20 b's each hold 22000
+    wedges, then 58900 ids of degree 20-21 (a circulant C2, 3000 of them with
+    one b) hold 3000.  A's first windowed-hash window (~29K ids by the
+    uniform estimate) holds ~23K wedges > kHashWinMax and is re-cut."""
+    rng = np.random.default_rng(seed)
+    nb, n1, n2 = 100, 1100, 58900
+    A = 0
+    bs = np.arange(1, 1 + nb)
+    c1 = np.arange(1 + nb, 1 + nb + n1)
+    c2 = np.arange(1 + nb + n1, 1 + nb + n1 + n2)
+    leaves = np.arange(c2[-1] + 1, c2[-1] + 1 + 200)
+    e = [np.stack([np.full(nb, A), bs], 1), np.stack([np.full(200, A), leaves], 1)]
+    for c in c1:
+        e.append(np.stack([rng.choice(bs, 20, replace=False), np.full(20, c)], 1))
+    i = np.arange(n2)
+    for d in range(1, 11):
+        e.append(np.stack([c2[i], c2[(i + d) % n2]], 1))
+    pick = rng.choice(n2, 3000, replace=False)
+    e.append(np.stack([rng.choice(bs, 3000), c2[pick]], 1))
+    return np.concatenate(e).astype(np.uint64)
+
+
+def test_sparse_big_recut(cuda_device, monkeypatch):
+    """Windowed-hash re-cut path (see recut_graph) against the oracle."""
+    monkeypatch.setenv("GL_SPARSE_BIG", "all")
+    pairs = recut_graph()
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+
+
 def test_hub_full_counters(cuda_device):
     """A hub with |L(a)| >= 65536 switches k_cycle_big to 32-bit counters
     (32K-id windows); leaves carry a sparse random graph plus a second hub so

@@ -268,11 +268,13 @@ __device__ __forceinline__ u64 dense_windows(u32 a, const unsigned* __restrict__
 }
 
 // Sparse big tops take the windowed hash when factor * (hash windows) <=
-// (dense windows).  GL_SPARSE_BIG=all|off overrides (tests force both paths).
+// (dense windows).  GL_SPARSE_BIG=all|off|<factor> overrides (tests force both
+// paths).
 inline u32 sparse_big_factor() {
     const char* e = std::getenv("GL_SPARSE_BIG");
     if (e && !std::strcmp(e, "all")) return 0u;
     if (e && !std::strcmp(e, "off")) return 0xffffffffu;
+    if (e && *e >= '0' && *e <= '9') return (u32)std::strtoul(e, nullptr, 10);
     return 4u;
 }
 

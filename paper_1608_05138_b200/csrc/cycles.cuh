@@ -532,6 +532,54 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
 
+        if constexpr (!WIN) {
+            // Hash tops take all c < a in one window: b's run is its whole row
+            // prefix N(b) n [0, a) (|.| = epos), so the runs are placed straight
+            // from (eu, epos) -- no cursors, no scratch round trips.
+            u32 my_runs = 0, my_wedges = 0;
+            for (u32 j = threadIdx.x; j < nb; j += THREADS) {
+                const u32 re = g.epos[E0 + j];
+                my_runs += re > 0;
+                my_wedges += re;
+            }
+            u64 tot, mine = ((u64)my_runs << 32) | my_wedges;
+            {
+                using BlockScan = cub::BlockScan<u64, THREADS>;
+                __shared__ typename BlockScan::TempStorage tmp;
+                BlockScan(tmp).ExclusiveSum(mine, mine, tot);
+            }
+            const u32 nnz = (u32)(tot >> 32), T = (u32)tot;
+            const RunMeta M = nnz <= kMeta ? Msm : Mgl;
+            u32 q = (u32)(mine >> 32), w = (u32)mine;
+            for (u32 j = threadIdx.x; j < nb && my_runs; j += THREADS) {
+                const u64 e = E0 + j;
+                const u32 re = g.epos[e];
+                if (!re) continue;
+                M.rj[q] = j;
+                M.rs[q] = (u32)g.off[g.eu[e]];
+                M.pre[q] = w;
+                ++q;
+                w += re;
+            }
+            if (threadIdx.x == 0) M.pre[nnz] = T;
+            if (threadIdx.x < 3) s_work[threadIdx.x] = 0;
+            __syncthreads();
+            GL_PROF_MARK(2);
+            GL_PROF_ADD(8, 1);
+            GL_PROF_ADD(9, T);
+            GL_PROF_ADD(10, 1);
+            if (T) {
+                meta_pass<KIND, 0>(g, Msm, Mgl, nnz, T, &s_work[0], W, 0, 1, abase, slot_acc);
+                __syncthreads();
+                GL_PROF_MARK(3);
+                meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, 0, 1, abase, slot_acc);
+                __syncthreads();
+                GL_PROF_MARK(4);
+                for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = i < kSlots ? kEmpty : 0u;
+            }
+            GL_PROF_SYNC_MARK(7);
+            continue;
+        }
         if (threadIdx.x == 0) {
             s_next = WIN ? kEmpty : 0u;
             s_rem = 0;

@@ -648,7 +648,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s2>>>(iout, nsparse + nbig + nmid + nsmid, nsmall, rank,
                                                                        world, lsmall);
                 GL_LAUNCH_CHECK();
-                const size_t smem = (size_t)kCycleSmallWarps * 2 * kHashSlots * sizeof(u32);
+                const size_t smem = (size_t)kCycleSmallWarps * kSmallWarpWords * sizeof(u32);
                 smem_attr(k_cycle_small, smem, gr.device);
                 k_cycle_small<<<(unsigned)sms * 3, kCycleSmallWarps * 32, smem, s2>>>(
                     g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, cs.slots.as<i64>());

@@ -10,18 +10,28 @@ __device__ __forceinline__ u32 hslot(u32 key) { return (key * 0x9E3779B1u) >> (3
 static_assert(kHashSlots == 1024, "hslot assumes 1024 slots");
 
 // Small tops: one warp per top vertex a, W[c] in a warp-private hash.
+// per-warp shared words of k_cycle_small: keys u32[kHashSlots], counts u16
+// packed in kHashSlots/2 words, the touched-slot list u16[kSmallWedges],
+// the list length, and for tops with nb <= kSmallLocalB the run table
+// pre u32[nb+1] (wedge prefix) and rbase u32[nb] (row base of b)
+constexpr u32 kSmallLocalB = 128;
+constexpr u32 kSmallWarpWords =
+    kHashSlots + kHashSlots / 2 + (u32)kSmallWedges / 2 + 1 + (kSmallLocalB + 1) + kSmallLocalB;
+
 __global__ void __launch_bounds__(kCycleSmallWarps * 32)
 k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ items, u64 n_items,
               unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc) {
     extern __shared__ u32 smem[];
     const u32 lane = lane_id();
     const u32 wib = threadIdx.x >> 5;
-    u32* keys = smem + wib * 2 * kHashSlots;
-    u32* cnt = keys + kHashSlots;
-    for (u32 i = lane; i < kHashSlots; i += 32) {
-        keys[i] = kEmpty;
-        cnt[i] = 0;
-    }
+    u32* keys = smem + wib * kSmallWarpWords;
+    u32* cnt = keys + kHashSlots; // two u16 counts per word
+    unsigned short* list = reinterpret_cast<unsigned short*>(cnt + kHashSlots / 2);
+    u32* nlist = cnt + kHashSlots / 2 + (u32)kSmallWedges / 2;
+    u32* pre = nlist + 1;
+    u32* rbase = pre + kSmallLocalB + 1;
+    for (u32 i = lane; i < kHashSlots; i += 32) keys[i] = kEmpty;
+    for (u32 i = lane; i < kHashSlots / 2; i += 32) cnt[i] = 0;
     __syncwarp();
     for (;;) {
         unsigned long long idx = 0;
@@ -30,49 +40,88 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
         if (idx >= n_items) break;
         const u32 a = items[idx];
         const u64 E0 = g.loff[a], E1 = g.loff[a + 1];
-        const u64 w0 = wpre[E0], w1 = wpre[E1];
-        const u32 nw = (u32)(w1 - w0);
-        // pass 1: W[c]++
+        const u32 nb = (u32)(E1 - E0);
+        const u64 w0 = wpre[E0];
+        const u32 nw = (u32)(wpre[E1] - w0);
+        // run table of the top in shared memory when small (the per-wedge run
+        // search is then LDS), else searched in wpre
+        const bool loc = nb <= kSmallLocalB;
+        if (loc) {
+            for (u32 j = lane; j < nb; j += 32) {
+                pre[j] = (u32)(wpre[E0 + j] - w0);
+                rbase[j] = (u32)g.off[g.eu[E0 + j]];
+            }
+            if (lane == 0) pre[nb] = nw;
+        }
+        if (lane == 0) *nlist = 0;
+        __syncwarp();
+        // wedge k -> (run j, adjacency slot)
+        auto locate = [&](u32 k, u32& j, u64& slot) {
+            if (loc) {
+                j = upper_bound_dev<u32, u32>(pre, 0, nb + 1, k) - 1;
+                slot = (u64)rbase[j] + (k - pre[j]);
+            } else {
+                const u64 gi = w0 + k;
+                const u64 e = upper_bound_dev<u64, u64>(wpre, E0, E1 + 1, gi) - 1;
+                j = (u32)(e - E0);
+                slot = g.off[g.eu[e]] + (gi - wpre[e]);
+            }
+        };
+        // pass 1: W[c]++; first inserts record their slot for the sparse clear
         for (u32 base = 0; base < nw; base += 32) {
-            u32 k = base + lane;
+            const u32 k = base + lane;
+            bool fresh = false;
+            u32 h = 0;
             if (k < nw) {
-                u64 gi = w0 + k;
-                u64 e = upper_bound_dev<u64, u64>(wpre, E0, E1 + 1, gi) - 1;
-                u32 b = g.eu[e];
-                u32 cv = g.adj[g.off[b] + (gi - wpre[e])];
-                u32 h = hslot(cv);
+                u32 j;
+                u64 slot;
+                locate(k, j, slot);
+                const u32 cv = g.adj[slot];
+                h = hslot(cv);
                 for (;;) {
-                    u32 prev = atomicCAS(&keys[h], kEmpty, cv);
-                    if (prev == kEmpty || prev == cv) break;
+                    const u32 prev = atomicCAS(&keys[h], kEmpty, cv);
+                    if (prev == kEmpty) {
+                        fresh = true;
+                        break;
+                    }
+                    if (prev == cv) break;
                     h = (h + 1) & (kHashSlots - 1);
                 }
-                atomicAdd(&cnt[h], 1u);
+                atomicAdd(&cnt[h >> 1], 1u << ((h & 1) << 4));
             }
+            const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+            const u32 at = *nlist; // every lane reads before lane 0 advances it
+            __syncwarp();
+            if (fresh) list[at + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)h;
+            if (lane == 0) *nlist = at + __popc(bal);
+            __syncwarp();
         }
-        __syncwarp();
         // pass 2: credit W[c]-1 to (b,c) and, summed per b, to (a,b)
         for (u32 base = 0; base < nw; base += 32) {
-            u32 k = base + lane;
-            u64 e = ~0ull, val = 0;
+            const u32 k = base + lane;
+            u32 j = 0xffffffffu;
+            u64 val = 0;
             if (k < nw) {
-                u64 gi = w0 + k;
-                e = upper_bound_dev<u64, u64>(wpre, E0, E1 + 1, gi) - 1;
-                u32 b = g.eu[e];
-                u64 slot = g.off[b] + (gi - wpre[e]);
-                u32 cv = g.adj[slot];
+                u64 slot;
+                locate(k, j, slot);
+                const u32 cv = g.adj[slot];
                 u32 h = hslot(cv);
                 while (keys[h] != cv) h = (h + 1) & (kHashSlots - 1);
-                val = cnt[h] - 1;
+                val = ((cnt[h >> 1] >> ((h & 1) << 4)) & 0xffffu) - 1u;
                 if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
             }
             u64 sum;
-            bool tail = seg_tail_sum(e, val, &sum);
-            if (k < nw && tail && sum) atomic_add_i64(&slot_acc[g.off[a] + (e - E0)], (i64)sum);
+            const bool tail = seg_tail_sum(j, val, &sum);
+            if (k < nw && tail && sum) atomic_add_i64(&slot_acc[g.off[a] + j], (i64)sum);
         }
         __syncwarp();
-        for (u32 i = lane; i < kHashSlots; i += 32) {
-            keys[i] = kEmpty;
-            cnt[i] = 0;
+        // sparse clear: only the slots this top filled (a count word is shared
+        // by slots h and h^1; both are either listed or already zero)
+        const u32 nl = *nlist;
+        for (u32 i = lane; i < nl; i += 32) {
+            const u32 h = list[i];
+            keys[h] = kEmpty;
+            cnt[h >> 1] = 0;
         }
         __syncwarp();
     }

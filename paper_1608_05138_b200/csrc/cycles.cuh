@@ -502,6 +502,14 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
     }
 }
 
+// Bulk reset of the first `words` table words (a multiple of 4) with 16-byte
+// stores: hash key words (< kslots) to kEmpty, counter words to 0.
+__device__ __forceinline__ void table_clear(u32* W, u32 words, u32 kslots, u32 threads) {
+    uint4* W4 = reinterpret_cast<uint4*>(W);
+    const uint4 e = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty), z = make_uint4(0, 0, 0, 0);
+    for (u32 i = threadIdx.x; i < words / 4; i += threads) W4[i] = 4 * i < kslots ? e : z;
+}
+
 // One pass over a window's runs.  Run metadata that did not fit in shared
 // memory (nnz > kMeta, written to the block's global scratch by the
 // compaction) is staged back through shared memory kMeta runs at a time, so
@@ -546,7 +554,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
     BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
     const RunMeta Msm{W + kWords, W + kWords + kMeta + 1, W + kWords + 2 * kMeta + 1};
     const RunMeta Mgl{S.pre, S.rs, S.rj};
-    for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
+    table_clear(W, kWords, HASH ? kSlots : 0u, THREADS);
 #ifdef GL_CYCLE_PROF
     // make prof: per-phase clock64 totals (thread 0, between barriers): 0 setup,
     // 6 gallop, 1 scan, 2 compaction, 3 pass 0, 4 pass 1, 7 clear, 5 grab;
@@ -624,7 +632,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, 0, 1, abase, slot_acc);
                 __syncthreads();
                 GL_PROF_MARK(4);
-                for (u32 i = threadIdx.x; i < kWords; i += THREADS) W[i] = i < kSlots ? kEmpty : 0u;
+                table_clear(W, kWords, kSlots, THREADS);
             }
             GL_PROF_SYNC_MARK(7);
             continue;
@@ -796,7 +804,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 GL_PROF_MARK(4);
                 if (bulk_clear) {
                     const u32 words = HASH ? kWords : (hi - lo + (1u << cl) - 1u) >> cl;
-                    for (u32 i = threadIdx.x; i < words; i += THREADS) W[i] = (HASH && i < kSlots) ? kEmpty : 0u;
+                    table_clear(W, (words + 3u) & ~3u, HASH ? kSlots : 0u, THREADS);
                 } else if (!HASH) {
                     meta_pass<KIND, 2>(g, Msm, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
                 }

@@ -7,4 +7,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.log 2>&1; echo bench rc=$?
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_${TAG}.log 2>&1; echo benchref rc=$?
+timeout 600 python bench.py --graph ba --steps 3 --warmup 3 > gpurun_out/bench_ba_${TAG}.log 2>&1; echo bench_ba rc=$?
 bash scripts/profile.sh ${TAG}

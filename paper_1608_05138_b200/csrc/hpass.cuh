@@ -610,8 +610,11 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // phase 2: stream the H-edges (kept in the device-wide list when it had room)
         const u32 nh = s_nh;
         if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
+        // the next record's load is in flight during this record's popcounts
+        uint2 nx = threadIdx.x < nh ? hout[threadIdx.x] : make_uint2(0u, 0u);
         for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
-            const uint2 he = hout[h];
+            const uint2 he = nx;
+            if (h + blockDim.x < nh) nx = hout[h + blockDim.x];
             const u32 i = he.x & 0xffffu, j = he.x >> 16;
             const u32* ri = rows + (u64)i * RS;
             const u32* rj = rows + (u64)j * RS;

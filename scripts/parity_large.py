@@ -2,7 +2,7 @@
 oracle's reference pipeline (16 host threads; minutes of CPU time), for the
 default cycle-kind choice and with the sparse-big choice forced both ways
 (GL_SPARSE_BIG=all / off).
-Usage: python scripts/parity_large.py [rmat:18 rmat:19 ba:500000:8 ...]
+Usage: python scripts/parity_large.py [rmat:18 rmat:20:1 ba:500000:8 ...] (rmat:<scale>[:<seed>])
 (default rmat:18 rmat:19); results are kept in profiles/*parity_large*.txt"""
 import os
 import sys
@@ -20,7 +20,7 @@ for spec in specs:
     kind, *args = spec.split(":")
     if kind == "rmat":
         sc = int(args[0])
-        pairs = gl.generate_rmat(sc, 16, seed=100 + sc)
+        pairs = gl.generate_rmat(sc, 16, seed=int(args[1]) if len(args) > 1 else 100 + sc)
     else:
         n, k = int(args[0]), int(args[1])
         pairs = gl.generate_ba(n, k, seed=7)

@@ -57,12 +57,16 @@ __device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 2k, >= 64 
     u32 l = 32 - __clz(2 * k - 1);
     return l < 6 ? 6 : l;
 }
+// bitmap row stride of H_a in u32 words: rows are read as u64 words with an
+// odd u64 stride, so the rows of different members fall in different banks
+// (phase 2 reads two arbitrary rows) and each popcount step covers 64 members
+__host__ __device__ inline u32 hrow_stride(u32 k) { return 2u * (((k + 63u) >> 6) | 1u); }
+
 __host__ __device__ inline u64 hpass_ws_words(u32 k, int mode, u32 bloom_w) {
     u32 l = 6;
     while ((1u << l) < 2 * k) ++l;
     const u64 H = 1ull << l;
-    const u64 W = (k + 31) / 32;
-    const u64 body = mode == 0 ? 2ull * k + (u64)k * (W | 1)  // xs, tri, rows (odd stride)
+    const u64 body = mode == 0 ? 2ull * k + (u64)k * hrow_stride(k)  // xs, tri, rows (8-byte aligned: 2k even)
                                : 4ull * k + 2;          // xs, ta, acc (u64, aligned)
     return body + 2 + H + H / 2 + bloom_w + 2ull * k; // + member list bounds
 }
@@ -434,9 +438,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     u32* rows = tri + k;                    // kHPassCount
     u32* ta = xs + k;                       // kHPassSums
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
-    // bitmap rows use an odd word stride RS so that the rows of different
-    // members fall in different banks (phase 2 reads two arbitrary rows)
-    const u32 RS = W | 1u;
+    const u32 RS = hrow_stride(k), W2 = (k + 63u) >> 6; // u32 stride, u64 words per row
     const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * RS : ((2ull * k + 1) & ~1ull) + 2ull * k;
     u32* bloom = ws + body;
     u32* hkey = bloom + bloom_words<BLOG>();
@@ -616,10 +618,10 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
             const uint2 he = nx;
             if (h + blockDim.x < nh) nx = hout[h + blockDim.x];
             const u32 i = he.x & 0xffffu, j = he.x >> 16;
-            const u32* ri = rows + (u64)i * RS;
-            const u32* rj = rows + (u64)j * RS;
+            const unsigned long long* ri = reinterpret_cast<const unsigned long long*>(rows + (u64)i * RS);
+            const unsigned long long* rj = reinterpret_cast<const unsigned long long*>(rows + (u64)j * RS);
             u32 c = 0;
-            for (u32 v = 0; v < W; ++v) c += __popc(ri[v] & rj[v]);
+            for (u32 v = 0; v < W2; ++v) c += __popcll(ri[v] & rj[v]);
             atomicAdd(&t[he.y], 1u);
             if (c) {
                 atomicAdd(&tri[i], c);
@@ -631,8 +633,8 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // phase 3: edges (a, x_i)
         for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
             u32 deg = 0;
-            const u32* ri = rows + (u64)i * RS;
-            for (u32 v = 0; v < W; ++v) deg += __popc(ri[v]);
+            const unsigned long long* ri = reinterpret_cast<const unsigned long long*>(rows + (u64)i * RS);
+            for (u32 v = 0; v < W2; ++v) deg += __popcll(ri[v]);
             const u32 e = g.eid[ub + i];
             if (deg) atomicAdd(&t[e], deg);
             if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));

@@ -729,20 +729,24 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                 // a KIND 3 window over its wedge cap: restore its b's cursors
                 // and re-cut it narrower (a window of <= kHashWinMax ids is
                 // always accepted: its distinct c ids fit the slots anyway)
-                if (!(KIND == 3 && T > kHashWinMax && hi - lo > kHashWinMax)) break;
+                if constexpr (KIND == 3) {
+                    if (T <= kHashWinMax || hi - lo <= kHashWinMax) break;
 #ifdef GL_CYCLE_PROF
-                if (threadIdx.x == 0) atomicAdd(&g_cycle_prof[29], 1ull); // KIND 3 re-cuts
+                    if (threadIdx.x == 0) atomicAdd(&g_cycle_prof[29], 1ull); // KIND 3 re-cuts
 #endif
-                for (u32 j = threadIdx.x; j < nb; j += THREADS) {
-                    if (S.rwin[j] != win) continue;
-                    const u32 c0 = S.hpos[j];
-                    S.cur[j] = c0;
-                    S.nextc[j] = g.adj[S.rb[j] + c0];
-                    S.rwin[j] = kEmpty;
+                    for (u32 j = threadIdx.x; j < nb; j += THREADS) {
+                        if (S.rwin[j] != win) continue;
+                        const u32 c0 = S.hpos[j];
+                        S.cur[j] = c0;
+                        S.nextc[j] = g.adj[S.rb[j] + c0];
+                        S.rwin[j] = kEmpty;
+                    }
+                    __syncthreads(); // BlockScan storage reuse
+                    const u64 nspan = (u64)(hi - lo) * kHashWinTarget / T;
+                    hi = lo + (u32)(nspan ? nspan : 1);
+                } else {
+                    break;
                 }
-                __syncthreads(); // BlockScan storage reuse
-                u64 nspan = (u64)(hi - lo) * kHashWinTarget / T;
-                hi = lo + (u32)(nspan ? nspan : 1);
             }
             rem -= T;
 #ifdef GL_CYCLE_PROF

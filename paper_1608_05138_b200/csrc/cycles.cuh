@@ -208,7 +208,7 @@ __device__ __forceinline__ u64 gallop_from(const u32* __restrict__ a, u64 lo, u6
 
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
 struct BigScratch {
-    u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin, *plen;
+    u32 *cur, *hpos, *rend, *pre, *rj, *rs, *nextc, *rwin, *plen, *lastc;
     u64* rb;
 };
 // compacted runs of one window: wedge prefix pre[nnz+1], first adjacency slot
@@ -229,9 +229,10 @@ __device__ __forceinline__ BigScratch big_scratch(u32* base, u32 cap) {
     s.nextc = reinterpret_cast<u32*>(s.rb + cap); // c at the cursor (kEmpty: row done)
     s.rwin = s.nextc + cap;                        // window of b's last recorded run
     s.plen = s.rwin + cap;                         // length of b's last run (search hint)
+    s.lastc = s.plen + cap;                        // last c of b's row prefix N(b) n [0, a)
     return s;
 }
-__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 11ull * cap + 8; }
+__host__ __device__ inline u64 big_scratch_words(u32 cap) { return 12ull * cap + 8; }
 
 
 // W[c] table of one block: dense window over c in [lo, lo+span) (big tops)
@@ -652,6 +653,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             S.rend[j] = re;
             S.cur[j] = 0;
             const u32 c = re > 0 ? g.adj[rb] : kEmpty;
+            if (WIN) S.lastc[j] = re > 0 ? g.adj[rb + re - 1] : 0u;
             S.nextc[j] = c;
             S.rwin[j] = kEmpty;
             S.plen[j] = 0;
@@ -704,7 +706,8 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                         const u32 c0 = S.cur[j], re = S.rend[j];
                         const u64 rb = S.rb[j];
                         u32 h = re;
-                        if (WIN) {
+                        // the row's last window needs no search: its run ends at re
+                        if (WIN && S.lastc[j] >= hi) {
                             const u32 pl = S.plen[j];
                             h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
                             S.plen[j] = h - c0;

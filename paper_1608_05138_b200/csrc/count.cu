@@ -427,6 +427,10 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     const u64 m = g.m, n = g.n;
     // adjacency slots are carried as u32 in the cycle run metadata
     if (2 * m >= (1ull << 32)) throw overflow_error("counting needs 2m < 2^32 adjacency slots (m < 2^31 edges)");
+    // A cycle pass of a previous count_begin that was never joined by
+    // count_mid is still writing the slot accumulators and reading the queue
+    // counters: finish it before any of them is reset below.
+    if (cs.s2) GL_CUDA(cudaStreamSynchronize(cs.s2));
     cs.launches = 0;
     cs.began = false;
     cs.mid_done = false;
@@ -449,7 +453,6 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
 
     // The H-pass (stream s) and the cycle pass (cs.s2, forked after the wedge
     // prefix) are independent and run concurrently; count_mid joins them.
-    if (cs.s2) GL_CUDA(cudaStreamSynchronize(cs.s2)); // a previous, un-joined cycle pass
     if (!cs.s2) {
         GL_CUDA(cudaStreamCreateWithFlags(&cs.s2, cudaStreamNonBlocking));
         for (int i = 0; i < 8; ++i) GL_CUDA(cudaEventCreate(&cs.ev[i]));

@@ -12,7 +12,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main(out_dir, scale):
+def make_pairs(gl, spec):
+    """rmat:<scale> (seed 3) or ba:<n>:<k>:<seed>"""
+    kind, *a = spec.split(":")
+    if kind == "rmat":
+        return gl.generate_rmat(int(a[0]), 16, seed=3)
+    return gl.generate_ba(int(a[0]), int(a[1]), seed=int(a[2]))
+
+
+def main(out_dir, spec):
     import torch
     import torch.distributed as dist
     import paper_1608_05138_b200 as gl
@@ -20,7 +28,7 @@ def main(out_dir, scale):
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
-    g = gl.Graph.build(gl.generate_rmat(scale, 16, seed=3), 0)
+    g = gl.Graph.build(make_pairs(gl, spec), 0)
     X, (b, e) = count_sharded(g, rank, world)
     rec = g.micro_records(b, e - b) if e > b else np.zeros(0, gl.MICRO_DTYPE)
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), rec)
@@ -30,4 +38,4 @@ def main(out_dir, scale):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]))
+    main(sys.argv[1], sys.argv[2])

@@ -238,41 +238,48 @@ def test_hub_full_counters(cuda_device):
     assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
 
 
-def test_sharded_equals_single(cuda_device):
-    """world=2 sharding emulated on one GPU: begin per rank, sum partial rows,
-    finish per shard, sum unrestricted -> identical macro and micro."""
+@pytest.mark.parametrize("graph,sparse,world", [("rmat12", None, 2), ("ba60k", None, 2), ("ba60k", "off", 2), ("ba60k", "all", 2), ("ba60k", "all", 3)])
+def test_sharded_equals_single(cuda_device, monkeypatch, graph, sparse, world):
+    """world=2/3 sharding emulated on one GPU: begin per rank, sum partial rows,
+    finish per shard, sum unrestricted -> identical macro and micro (BA 60k
+    with GL_SPARSE_BIG=all: the windowed-hash tops are split across ranks)."""
     import torch
-    pairs = gl.generate_rmat(12, 16, seed=5)
+    if sparse:
+        monkeypatch.setenv("GL_SPARSE_BIG", sparse)
+    pairs = gl.generate_rmat(12, 16, seed=5) if graph == "rmat12" else gl.generate_ba(60000, 6, seed=3)
     g = gl.Graph.build(pairs, cuda_device)
     full = g.count()
     full_rec = g.micro_records()
-    world = 2
     plen = g.partials_len(world)
     parts, tris = [], []
-    for rank in range(world):
-        buf = torch.empty(2 * plen, dtype=torch.int64, device="cuda")
-        g.count_begin(rank, world, buf.data_ptr())
-        ptr, m = g.triangle_counts_device()
-        tris.append(_copy_u32(ptr, m))
-        parts.append(buf)
-    # all-reduce of t (emulated), then each rank's share of the triangle sums
-    tsum = tris[0] + tris[1]
-    for rank in range(world):
-        g.count_begin(rank, world, parts[rank].data_ptr())
-        ptr, m = g.triangle_counts_device()
-        _write_u32(ptr, tsum)
-        g.count_mid(parts[rank].data_ptr())
-    total = parts[0] + parts[1]
+    # every library call and every torch op on one stream, as in dist.sharded_step
+    # (the library's own stream is non-blocking: torch's default stream would race it)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for rank in range(world):
+            buf = torch.empty(2 * plen, dtype=torch.int64, device="cuda")
+            g.count_begin(rank, world, buf.data_ptr(), st.cuda_stream)
+            ptr, m = g.triangle_counts_device()
+            tris.append(_copy_u32(ptr, m))
+            parts.append(buf)
+        # all-reduce of t (emulated), then each rank's share of the triangle sums
+        tsum = sum(tris[1:], tris[0])
+        for rank in range(world):
+            g.count_begin(rank, world, parts[rank].data_ptr(), st.cuda_stream)
+            ptr, m = g.triangle_counts_device()
+            _write_u32(ptr, tsum)
+            g.count_mid(parts[rank].data_ptr(), st.cuda_stream)
+        total = sum(parts[1:], parts[0])
+        from paper_1608_05138_b200.dist import shard_range
+        Csum = [0] * 17
+        recs = []
+        for rank in range(world):
+            b, e = shard_range(g.num_edges(), world, rank)
+            shard = total[2 * b:2 * e].contiguous()
+            Cr = g.count_finish(shard.data_ptr(), b, e, st.cuda_stream)
+            Csum = [x + y for x, y in zip(Csum, Cr)]
+            recs.append(g.micro_records(b, e - b))
     torch.cuda.synchronize()
-    from paper_1608_05138_b200.dist import shard_range
-    Csum = [0] * 17
-    recs = []
-    for rank in range(world):
-        b, e = shard_range(g.num_edges(), world, rank)
-        shard = total[2 * b:2 * e].contiguous()
-        Cr = g.count_finish(shard.data_ptr(), b, e)
-        Csum = [x + y for x, y in zip(Csum, Cr)]
-        recs.append(g.micro_records(b, e - b))
     assert gl.global_from_unrestricted(Csum, g.num_vertices(), g.num_edges()) == full.X
     assert Csum == full.C
     assert np.array_equal(np.concatenate(recs), full_rec)
@@ -367,7 +374,8 @@ def test_cli_count_spec_examples(tmp_path):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_ranks_share_gpu(cuda_device, tmp_path, world):
+@pytest.mark.parametrize("spec", ["rmat:13", "ba:60000:6:3"])
+def test_sharded_ranks_share_gpu(cuda_device, tmp_path, world, spec):
     """The multi-rank path end to end: `world` processes (torchrun, gloo, all on
     cuda:0) each count their cost-balanced share, exchange t / partial rows /
     128-bit sums, and finalise their edge shard; the shards' micro records and
@@ -375,13 +383,13 @@ def test_sharded_ranks_share_gpu(cuda_device, tmp_path, world):
     import json
     import subprocess
     import sys
-    scale = 13
-    pairs = gl.generate_rmat(scale, 16, seed=3)
+    from _dist_worker import make_pairs
+    pairs = make_pairs(gl, spec)
     g, res, rec = gpu_count(pairs, cuda_device)
     worker = os.path.join(os.path.dirname(__file__), "_dist_worker.py")
     subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                     "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), worker, str(tmp_path),
-                    str(scale)], check=True, timeout=600, capture_output=True)
+                    spec], check=True, timeout=600, capture_output=True)
     shards, xs = [], []
     for r in range(world):
         shards.append(np.load(tmp_path / f"rank{r}.npy"))

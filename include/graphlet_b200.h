@@ -139,7 +139,11 @@ int gl_count(gl_graph *g, gl_graphlet_vector *X, gl_unrestricted *unres);
  *     epilogue for that shard, micro records on device, unrestricted
  *     partial sums in *unres.
  *  6. caller sums unres across ranks (e.g. as 32-bit limbs in int64) and
- *     calls gl_global_from_unrestricted. */
+ *     calls gl_global_from_unrestricted.
+ * Steps 1-5 are asynchronous on `stream` (NULL: the graph's own stream); the
+ * caller's collectives belong on the same stream or must wait for it.
+ * gl_count_begin may be called again before gl_count_mid (it first drains the
+ * previous call's cycle pass). */
 uint64_t gl_partials_len(const gl_graph *g, int world);
 int gl_count_begin(gl_graph *g, int rank, int world, int64_t *d_partials, void *stream);
 int gl_triangle_counts_device(gl_graph *g, uint32_t **d_t, uint64_t *count);

@@ -106,12 +106,29 @@ __global__ void k_edge_keys(const u64* __restrict__ pairs, u64 count, const u64*
     }
 }
 
+// Degrees from the sorted canonical keys (x << vb | y, x < y): the x side
+// comes in runs (one per lower endpoint), so each warp adds a run's length
+// with one atomic (the hubs of skewed graphs are mostly x: no contention on
+// their counter); the y side is one atomic per edge.
 __global__ void k_degree(const u64* __restrict__ keys, u64 m, int vb, u32* __restrict__ deg) {
     const u64 mask = ((u64)1 << vb) - 1;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
-        u64 k = keys[i];
-        atomicAdd(&deg[k >> vb], 1u);
-        atomicAdd(&deg[k & mask], 1u);
+    const u32 lane = threadIdx.x & 31u;
+    for (u64 base = blockIdx.x * (u64)blockDim.x + (threadIdx.x & ~31u); base < m;
+         base += (u64)gridDim.x * blockDim.x) {
+        const u64 i = base + lane;
+        const bool valid = i < m;
+        const u64 k = valid ? keys[i] : 0;
+        const u32 x = valid ? (u32)(k >> vb) : 0xffffffffu; // ids < n < 2^32 - 1
+        const u32 px = __shfl_up_sync(0xffffffffu, x, 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || px != x);
+        if (valid) {
+            if ((heads >> lane) & 1u) {
+                const unsigned later = heads & ~((2u << lane) - 1u); // 2u << 31 == 0: none
+                const u32 end = later ? (u32)__ffs(later) - 1u : 32u;
+                atomicAdd(&deg[x], end - lane);
+            }
+            atomicAdd(&deg[k & mask], 1u);
+        }
     }
 }
 

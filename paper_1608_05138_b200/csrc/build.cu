@@ -87,16 +87,23 @@ __global__ void k_max_label(const u64* __restrict__ p, u64 n, unsigned long long
 }
 
 // compact both endpoints by binary search in the unique label array
+// dense label range: label -> compact id table (one scatter), so the edge
+// keys take two loads per pair instead of two binary searches
+__global__ void k_label_table(const u64* __restrict__ labels, u64 n, u32* __restrict__ tab) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        tab[labels[i]] = (u32)i;
+}
+
 __global__ void k_edge_keys(const u64* __restrict__ pairs, u64 count, const u64* __restrict__ labels,
-                            u64 n, u64 sentinel, int vb, u64* __restrict__ keys) {
+                            const u32* __restrict__ tab, u64 n, u64 sentinel, int vb, u64* __restrict__ keys) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
         u64 a = pairs[2 * i], b = pairs[2 * i + 1];
         if (a == b) {
             keys[i] = sentinel;
             continue;
         }
-        u64 x = lower_bound_dev<u64, u64>(labels, 0, n, a);
-        u64 y = lower_bound_dev<u64, u64>(labels, 0, n, b);
+        u64 x = tab ? tab[a] : lower_bound_dev<u64, u64>(labels, 0, n, a);
+        u64 y = tab ? tab[b] : lower_bound_dev<u64, u64>(labels, 0, n, b);
         if (x > y) {
             u64 t = x;
             x = y;
@@ -235,12 +242,11 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         u64 nlab = 2 * count;
         lab_a.alloc(nlab * sizeof(u64));
         lab_b.alloc(nlab * sizeof(u64));
-        u64 n = 0;
+        u64 n = 0, maxlab = 0;
         if (count > 0) {
             GL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u64), s));
             k_max_label<<<grid_for(nlab), kThreads, 0, s>>>(d_pairs, nlab, (unsigned long long*)cnt);
             GL_LAUNCH_CHECK();
-            u64 maxlab = 0;
             GL_CUDA(cudaMemcpyAsync(&maxlab, cnt, sizeof(u64), cudaMemcpyDeviceToHost, s));
             GL_CUDA(cudaStreamSynchronize(s));
             sort_keys<u64>(tmp, const_cast<u64*>(d_pairs), lab_b.as<u64>(), nlab, bits_for(maxlab), s);
@@ -250,6 +256,14 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         lab_b.reset();
         const u64* labels = lab_a.as<u64>();
         const int vb = bits_for(n ? n - 1 : 0);
+        DevBuf ltab;
+        const u32* tab = nullptr;
+        if (n && maxlab < (1ull << 28) && maxlab <= 4 * n + (1ull << 20)) {
+            ltab.alloc((maxlab + 1) * sizeof(u32));
+            k_label_table<<<grid_for(n), kThreads, 0, s>>>(labels, n, ltab.as<u32>());
+            GL_LAUNCH_CHECK();
+            tab = ltab.as<u32>();
+        }
 
         // 2. canonical undirected keys
         DevBuf keys_a, keys_b;
@@ -261,7 +275,7 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         const u64 sentinel = kb >= 64 ? ~0ull : (((u64)1 << kb) - 1);
         u64 m = 0;
         if (count > 0) {
-            k_edge_keys<<<grid_for(count), kThreads, 0, s>>>(d_pairs, count, labels, n, sentinel, vb,
+            k_edge_keys<<<grid_for(count), kThreads, 0, s>>>(d_pairs, count, labels, tab, n, sentinel, vb,
                                                                keys_a.as<u64>());
             GL_LAUNCH_CHECK();
             sort_keys<u64>(tmp, keys_a.as<u64>(), keys_b.as<u64>(), count, kb, s);
@@ -276,6 +290,7 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         }
         if (m >= 0xffffffffull) throw overflow_error("graph exceeds 32-bit edge id space");
         keys_b.reset();
+        ltab.reset();
         const u64* ekeys = keys_a.as<u64>();
 
         // 3. degrees + P1 relabel

@@ -57,8 +57,8 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--e2e-warmup", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-warmup", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 

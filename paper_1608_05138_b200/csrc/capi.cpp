@@ -335,9 +335,17 @@ int gl_edge_counts(const gl_graph* g, uint64_t first, uint64_t count, uint32_t* 
         if (first < cs.shard_begin || first + count > cs.shard_end)
             throw gl::invalid_argument("edge range outside the computed shard");
         GL_CUDA(cudaSetDevice(gr.device));
-        if (t) d2h(t, cs.t.as<uint32_t>() + first, count, gr.stream);
-        if (x7) d2h(x7, cs.x7.as<uint64_t>() + first, count, gr.stream);
-        if (x10) d2h(x10, cs.x10.as<uint64_t>() + first, count, gr.stream);
+        // the three copies queue back to back, one synchronisation
+        if (count && t)
+            GL_CUDA(cudaMemcpyAsync(t, cs.t.as<uint32_t>() + first, count * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                    gr.stream));
+        if (count && x7)
+            GL_CUDA(cudaMemcpyAsync(x7, cs.x7.as<uint64_t>() + first, count * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    gr.stream));
+        if (count && x10)
+            GL_CUDA(cudaMemcpyAsync(x10, cs.x10.as<uint64_t>() + first, count * sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, gr.stream));
+        GL_CUDA(cudaStreamSynchronize(gr.stream));
     });
 }
 

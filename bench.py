@@ -79,11 +79,29 @@ def workload(args):
             "scale": args.scale, "edge_factor": args.edge_factor}
 
 
+def workload_key(args):
+    """Key of this workload in profiles/traffic.json (ncu DRAM bytes per workload)."""
+    if args.graph == "ba":
+        return f"ba{args.ba_n}_{args.ba_attach}_s{args.seed}"
+    return f"rmat{args.scale}_ef{args.edge_factor}_s{args.seed}"
+
+
 def host_pairs(args):
     import paper_1608_05138_b200 as gl
     if args.graph == "ba":
         return gl.generate_ba(args.ba_n, args.ba_attach, seed=args.seed)
     return gl.generate_rmat(args.scale, args.edge_factor, seed=args.seed)
+
+
+def oracle_pairs(args):
+    """The same pairs from the oracle's generator ports (oracle.c, pinned equal
+    to the product's generators by tests/test_oracle.py): the reference arm
+    never loads the product library."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # CPU checker / baseline only
+    if args.graph == "ba":
+        return O.generate_ba(args.ba_n, args.ba_attach, seed=args.seed)
+    return O.generate_rmat(args.scale, args.edge_factor, seed=args.seed)
 
 
 # --------------------------------------------------------------------- clocks
@@ -177,7 +195,7 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
-    pairs = host_pairs(args)
+    pairs = oracle_pairs(args)
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     rates, cores, kind, desc = cpu_sample_run(pairs, per_step, steps=args.steps + args.warmup)
     rates = rates[args.warmup:] or rates
@@ -303,11 +321,14 @@ def run_ours(args):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bytes_alg[dom] / (phase_serial[dom] / 1e3) / 1e9 if phase_serial[dom] > 0 else 0.0
-    traffic = None
+    # DRAM bytes of the dominant kernel from an ncu capture OF THIS WORKLOAD
+    # (profiles/traffic.json, keyed by workload); null when none was taken
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(names[dom])
+            ent = json.load(open(tpath)).get("workloads", {}).get(workload_key(args), {})
+            traffic, traffic_src = ent.get(names[dom]), ent.get("source")
         except Exception:
             traffic = None
 
@@ -321,6 +342,11 @@ def run_ours(args):
         pin_x7 = torch.empty(max(1, shard_n), dtype=torch.int64).pin_memory()
         pin_x10 = torch.empty(max(1, shard_n), dtype=torch.int64).pin_memory()
         e2e_ms = []
+        # second variant: the reference caller's full per-edge output, every
+        # 80-byte MicroRecord (counts.hpp:82-89) of the shard, into pinned memory
+        pin_rec = torch.empty(max(1, shard_n) * 80, dtype=torch.uint8).pin_memory()
+        rec_view = pin_rec.numpy().view(gl.MICRO_DTYPE)[:shard_n]
+        rec_ms = []
         for i in range(args.e2e_steps + args.e2e_warmup):
             barrier()
             torch.cuda.synchronize()
@@ -332,23 +358,44 @@ def run_ours(args):
             g2.edge_counts(b, shard_n, pin_t.numpy().view(np.uint32)[:shard_n],
                            pin_x7.numpy().view(np.uint64)[:shard_n], pin_x10.numpy().view(np.uint64)[:shard_n])
             dt = (time.perf_counter() - t0) * 1e3
+            # same step again on the same graph object, ending in the full
+            # MicroRecord table instead of the compact (t, x7, x10) arrays
+            barrier()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            g3 = gl.Graph.build_host_ptr(pin_in.data_ptr(), count, local)
+            p3 = torch.empty(2 * g3.partials_len(world), dtype=torch.int64, device=dev)
+            X3, _ = sharded_step(g3, p3, rank, world, stream)
+            g3.micro_records(b, shard_n, out=rec_view)
+            dr = (time.perf_counter() - t1) * 1e3
             if os.environ.get("GL_BENCH_VERBOSE"):
-                print(f"e2e iteration {i}: {dt:.1f} ms", file=sys.stderr, flush=True)
+                print(f"e2e iteration {i}: {dt:.1f} ms, with micro records {dr:.1f} ms", file=sys.stderr, flush=True)
             g2.close()
-            del p2
+            g3.close()
+            del p2, p3
             if i >= args.e2e_warmup:  # warm-up iterations: first-touch allocations
                 e2e_ms.append(dt)
-            assert X2 == X, "e2e counts differ from device-resident counts"
-        tot = sum(e2e_ms)
+                rec_ms.append(dr)
+            assert X2 == X and X3 == X, "e2e counts differ from device-resident counts"
+        tot, tot_rec = sum(e2e_ms), sum(rec_ms)
         if world > 1:
-            t = torch.tensor([tot], dtype=torch.float64, device=dev)
+            t = torch.tensor([tot, tot_rec], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            tot = float(t.item())
+            tot, tot_rec = (float(x) for x in t.tolist())
         e2e = {"value": m * len(e2e_ms) / (tot / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(pin_in.numel() * 8),
                "d2h_bytes_per_step": int(shard_n * (4 + 8 + 8) + 18 * 16),
                "ms_per_step": tot / max(1, len(e2e_ms)),
-               "includes": "H2D of raw pairs, on-device CSR build, count, D2H of t/x7/x10 per edge + X"}
+               "includes": "H2D of the raw label pairs, on-device CSR build, count, D2H of the COMPACT per-edge "
+                           "output (t u32, x7 u64, x10 u64 = 20 B/edge; the other MicroRecord fields are "
+                           "closed-form in t and the degrees, counts.cpp:113-136) + X",
+               "micro_records": {
+                   "value": m * len(rec_ms) / (tot_rec / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(pin_in.numel() * 8),
+                   "d2h_bytes_per_step": int(shard_n * 80 + 18 * 16),
+                   "ms_per_step": tot_rec / max(1, len(rec_ms)),
+                   "includes": "same step ending in the full 80-byte MicroRecord table (micro_counts, "
+                               "counts.cpp:122-136) of every edge, D2H into pinned memory"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -372,6 +419,7 @@ def run_ours(args):
                          "duration_source": "CUDA events around the pass, one extra untimed step with the passes "
                                             "serialised (gl_set_overlap(0))",
                          "unit": "GB/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": bytes_alg[dom],
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650"},
             "phase_ms": {k: float(v) for k, v in zip(names + ["sum"], phase_ms)},

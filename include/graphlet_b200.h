@@ -24,12 +24,12 @@ extern "C" {
 
 /* ---- error codes (reference exception class in parentheses) ---- */
 #define GL_OK 0
-#define GL_ERR_INVALID -1     /* std::invalid_argument                              */
+#define GL_ERR_INVALID -1     /* std::invalid_argument (incl. >= 2^32-1 vertices or edges, graph.cpp:103-104) */
 #define GL_ERR_PARSE -2       /* graphlet::parse_error           (graph.hpp:23-33)  */
 #define GL_ERR_IO -3          /* std::runtime_error "cannot open" (graph.cpp:87-91) */
 #define GL_ERR_CUDA -4        /* device failure / no CUDA device / ext. missing      */
 #define GL_ERR_CONSISTENCY -5 /* graphlet::count_consistency_error (counts.hpp:13-16)*/
-#define GL_ERR_OVERFLOW -6    /* graphlet::count_overflow_error, 32-bit id space     */
+#define GL_ERR_OVERFLOW -6    /* graphlet::count_overflow_error (128-bit sums, 16-bit H-member ids) */
 #define GL_ERR_OOM -7         /* device allocation failed                           */
 #define GL_ERR_STATE -8       /* call sequence violated (e.g. finish before begin)  */
 

@@ -502,3 +502,128 @@ int or_brute_force_global(const or_graph *g, uint32_t cap, uint64_t X[36]) {
     store128(X, x, 18);
     return 0;
 }
+
+/* ------------------------------------------------------------ generators */
+/* Ports of the product's deterministic synthetic generators
+ * (paper_1608_05138_b200/csrc/common.cuh mix64/hash2/rmat_edge and
+ * csrc/host.cpp make_rmat_params/generate_ba), so that bench.py's reference
+ * arm and the fixture scripts build the same graphs WITHOUT loading the
+ * product library.  tests/test_oracle.py pins them equal to the product's. */
+
+static uint64_t g_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint64_t g_hash2(uint64_t seed, uint64_t ctr) { return g_mix64(seed ^ g_mix64(ctr)); }
+static uint32_t g_threshold(double x) {
+    double v = x * 4294967296.0;
+    if (v >= 4294967295.0) return 0xffffffffu;
+    return (uint32_t)v;
+}
+
+typedef struct {
+    uint32_t scale, ta, tb, tc;
+    uint64_t seed, count;
+    uint64_t *out;
+    int part, parts;
+} rmat_job;
+
+static void *rmat_worker(void *p) {
+    rmat_job *j = (rmat_job *)p;
+    uint64_t lo = j->count * (uint64_t)j->part / (uint64_t)j->parts;
+    uint64_t hi = j->count * (uint64_t)(j->part + 1) / (uint64_t)j->parts;
+    for (uint64_t i = lo; i < hi; ++i) {
+        uint64_t r = 0, c = 0;
+        for (uint32_t l = 0; l < j->scale; ++l) {
+            uint32_t x = (uint32_t)(g_hash2(j->seed, i * 64 + l) >> 32);
+            r <<= 1;
+            c <<= 1;
+            if (x < j->ta) {
+            } else if (x < j->tb) {
+                c |= 1;
+            } else if (x < j->tc) {
+                r |= 1;
+            } else {
+                r |= 1;
+                c |= 1;
+            }
+        }
+        j->out[2 * i] = r;
+        j->out[2 * i + 1] = c;
+    }
+    return NULL;
+}
+
+int or_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c, uint64_t seed,
+                     int nthreads, uint64_t *out) {
+    if (scale == 0 || scale > 40 || a < 0 || b < 0 || c < 0 || a + b + c > 1.0) return -1;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    rmat_job jobs[256];
+    uint64_t count = (uint64_t)edge_factor << scale;
+    for (int t = 0; t < nthreads; ++t) {
+        rmat_job j = {scale, g_threshold(a), g_threshold(a + b), g_threshold(a + b + c), seed, count, out, t, nthreads};
+        jobs[t] = j;
+        pthread_create(&th[t], NULL, rmat_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    return 0;
+}
+
+static uint64_t g_bounded(uint64_t h, uint64_t n) { return (uint64_t)(((u128)h * n) >> 64); }
+
+/* Barabasi-Albert: vertices 0..k form a clique, every later vertex attaches k
+ * distinct targets drawn from the endpoint list.  *out is malloc'd (2*count
+ * labels), freed with or_free_pairs. */
+int or_generate_ba(uint64_t n, uint32_t k, uint64_t seed, uint64_t **out, uint64_t *count) {
+    *out = NULL;
+    *count = 0;
+    if (k == 0) return -1;
+    if (n == 0) return 0;
+    uint64_t n0 = n < (uint64_t)k + 1 ? n : (uint64_t)k + 1;
+    uint64_t cap = n0 * (n0 - 1) / 2 + (n - n0) * (uint64_t)k;
+    uint64_t *pairs = (uint64_t *)malloc((2 * cap + 2) * sizeof(uint64_t));
+    uint64_t *ends = (uint64_t *)malloc((2 * cap + 2) * sizeof(uint64_t));
+    uint64_t *picked = (uint64_t *)malloc((uint64_t)k * sizeof(uint64_t));
+    if (!pairs || !ends || !picked) {
+        free(pairs);
+        free(ends);
+        free(picked);
+        return -1;
+    }
+    uint64_t np = 0, ne = 0, ctr = 0;
+    for (uint64_t x = 0; x < n0; ++x)
+        for (uint64_t y = x + 1; y < n0; ++y) {
+            pairs[2 * np] = y;
+            pairs[2 * np + 1] = x;
+            ++np;
+            ends[ne++] = x;
+            ends[ne++] = y;
+        }
+    for (uint64_t v = n0; v < n; ++v) {
+        uint32_t np_ = 0;
+        while (np_ < k) {
+            uint64_t w = ends[g_bounded(g_hash2(seed, ctr++), ne)];
+            int dup = 0;
+            for (uint32_t q = 0; q < np_; ++q) dup |= picked[q] == w;
+            if (!dup) picked[np_++] = w;
+        }
+        for (uint32_t q = 0; q < k; ++q) {
+            pairs[2 * np] = v;
+            pairs[2 * np + 1] = picked[q];
+            ++np;
+            ends[ne++] = v;
+            ends[ne++] = picked[q];
+        }
+    }
+    free(ends);
+    free(picked);
+    *out = pairs;
+    *count = np;
+    return 0;
+}
+
+void or_free_pairs(uint64_t *p) { free(p); }

@@ -68,6 +68,14 @@ int or_brute_force_global(const or_graph *g, uint32_t cap, uint64_t X[36]);
  * holds C_i (indices 3..16 used).  Returns -1 on inexact/negative. */
 int or_global_from_unrestricted(const uint64_t C[34], uint64_t n, uint64_t m, uint64_t X[36]);
 
+/* Ports of the product's synthetic generators (csrc/common.cuh rmat_edge,
+ * csrc/host.cpp generate_ba): identical pairs, no product library needed.
+ * or_generate_rmat writes 2*(edge_factor << scale) labels into out. */
+int or_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c, uint64_t seed,
+                     int nthreads, uint64_t *out);
+int or_generate_ba(uint64_t n, uint32_t k, uint64_t seed, uint64_t **out, uint64_t *count);
+void or_free_pairs(uint64_t *p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,13 @@ class Oracle:
             L.or_brute_force_global.restype = C.c_int
             L.or_global_from_unrestricted.argtypes = [vp, C.c_uint64, C.c_uint64, vp]
             L.or_global_from_unrestricted.restype = C.c_int
+            L.or_generate_rmat.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                           C.c_uint64, C.c_int, vp]
+            L.or_generate_rmat.restype = C.c_int
+            L.or_generate_ba.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.POINTER(C.c_uint64)),
+                                         C.POINTER(C.c_uint64)]
+            L.or_generate_ba.restype = C.c_int
+            L.or_free_pairs.argtypes = [vp]
             cls._lib = L
         return cls._lib
 
@@ -163,6 +170,33 @@ def global_from_unrestricted(Cs, n, m):
     return _x_from(X)
 
 
+def generate_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+                  seed: int = 1, threads: int = 0) -> np.ndarray:
+    """(count, 2) uint64 labels, identical to the product's gl_generate_rmat."""
+    L = Oracle.lib()
+    count = edge_factor << scale
+    out = np.empty((count, 2), np.uint64)
+    if L.or_generate_rmat(scale, edge_factor, a, b, c, seed, threads or (os.cpu_count() or 1), out.ctypes.data):
+        raise ValueError("bad RMAT parameters")
+    return out
+
+
+def generate_ba(n: int, attach: int, seed: int = 1) -> np.ndarray:
+    """(count, 2) uint64 labels, identical to the product's gl_generate_ba."""
+    L = Oracle.lib()
+    p = C.POINTER(C.c_uint64)()
+    cnt = C.c_uint64()
+    if L.or_generate_ba(n, attach, seed, C.byref(p), C.byref(cnt)):
+        raise ValueError("bad BA parameters")
+    k = int(cnt.value)
+    if k == 0:
+        return np.zeros((0, 2), np.uint64)
+    try:
+        return np.ctypeslib.as_array(p, shape=(2 * k,)).copy().reshape(k, 2)
+    finally:
+        L.or_free_pairs(p)
+
+
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
@@ -201,6 +235,8 @@ class RefLib:
             L.ref_brute.restype = C.c_int
             L.ref_brute_edges.argtypes = [vp, vp]
             L.ref_last_error.restype = C.c_char_p
+            L.ref_edges.argtypes = [vp, C.c_int, vp, C.c_uint64, vp]
+            L.ref_edges.restype = C.c_int
             cls._lib = L
         return cls._lib
 
@@ -250,6 +286,15 @@ class RefLib:
         if rc != 0:
             raise ArithmeticError(self.lib().ref_last_error().decode())
         return (_x_from(X), rec) if micro else _x_from(X)
+
+    def edges(self, edge_ids, threads: int = 1):
+        """The reference's process_edge_hash for the listed edge ids:
+        (k, 7) rows {v label, u label, t, s_u, s_v, x7, x10}."""
+        ids = np.ascontiguousarray(edge_ids, dtype=np.uint64)
+        out = np.zeros((len(ids), 7), np.uint64)
+        if self.lib().ref_edges(self.h, threads, ids.ctypes.data, len(ids), out.ctypes.data) != 0:
+            raise RuntimeError(self.lib().ref_last_error().decode())
+        return out
 
     def time_sample(self, edge_ids, threads: int):
         ids = np.ascontiguousarray(edge_ids, dtype=np.uint64)

@@ -212,6 +212,43 @@ double ref_time_sample(void* h, int nthreads, const std::uint64_t* ids, std::uin
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// The reference's per-edge pipeline (process_edge_hash, kernels.cpp:143-156)
+// for the listed oriented edge ids, nthreads workers; out = k rows of
+// {v label, u label, t, s_u, s_v, x7, x10} (labels = original vertex labels,
+// so a fixture also pins which edge an id names).
+int ref_edges(void* h, int nthreads, const std::uint64_t* ids, std::uint64_t k, std::uint64_t* out) {
+    auto* rg = static_cast<RefGraph*>(h);
+    try {
+        const std::uint64_t n = rg->g.num_vertices(), m = rg->g.num_edges();
+        for (std::uint64_t i = 0; i < k; ++i)
+            if (ids[i] >= m) throw std::out_of_range("edge id out of range");
+        if (nthreads < 1) nthreads = 1;
+        std::atomic<std::uint64_t> next{0};
+        std::vector<std::thread> th;
+        for (int w = 0; w < nthreads; ++w)
+            th.emplace_back([&] {
+                StampTable psi(n);
+                NeighborhoodSets sets;
+                sets.reserve(rg->g.max_degree());
+                for (;;) {
+                    const std::uint64_t i = next.fetch_add(1);
+                    if (i >= k) break;
+                    const OrientedEdge& e = rg->edges[ids[i]];
+                    EdgeMotifRecord r = process_edge_hash(rg->g, psi, e, sets);
+                    std::uint64_t* o = out + 7 * i;
+                    o[0] = rg->g.original_label(e.v);
+                    o[1] = rg->g.original_label(e.u);
+                    o[2] = r.t; o[3] = r.s_u; o[4] = r.s_v; o[5] = r.x7; o[6] = r.x10;
+                }
+            });
+        for (auto& t : th) t.join();
+        return 0;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
+    }
+}
+
 int ref_brute(void* h, std::uint32_t cap, std::uint64_t* X) {
     auto* rg = static_cast<RefGraph*>(h);
     try {

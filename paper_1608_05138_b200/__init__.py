@@ -378,19 +378,41 @@ class Graph:
         return [_to_int(uc.c[i]) for i in range(17)]
 
     # per-edge output ---------------------------------------------------------
-    def micro_records(self, first: int = 0, count: int | None = None) -> np.ndarray:
+    def micro_records(self, first: int = 0, count: int | None = None, out=None) -> np.ndarray:
+        """micro_counts (counts.cpp:122-136) rows of edge ids [first, first+count);
+        `out`: optional caller buffer (e.g. a pinned host array) of MICRO_DTYPE."""
         if count is None:
             count = self.num_edges() - first
-        out = np.zeros(count, dtype=MICRO_DTYPE)
+        if first < 0 or count < 0:
+            raise ValueError("negative edge range")
+        if out is None:
+            out = np.zeros(count, dtype=MICRO_DTYPE)
+        elif (not isinstance(out, np.ndarray) or out.dtype != MICRO_DTYPE or not out.flags.c_contiguous
+              or out.size < count or not out.flags.writeable):
+            raise ValueError(f"out: need a writeable C-contiguous MICRO_DTYPE array of >= {count} rows")
         _check(LIB.gl_micro_records(self._h, first, count, out.ctypes.data_as(C.c_void_p)))
         return out
 
     def edge_counts(self, first: int = 0, count: int | None = None, t=None, x7=None, x10=None):
         if count is None:
             count = self.num_edges() - first
-        t = np.zeros(count, dtype=np.uint32) if t is None else t
-        x7 = np.zeros(count, dtype=np.uint64) if x7 is None else x7
-        x10 = np.zeros(count, dtype=np.uint64) if x10 is None else x10
+        if first < 0 or count < 0:
+            raise ValueError("negative edge range")
+
+        def out(a, dt, name):
+            # caller buffers are written through raw pointers: insist on the
+            # exact dtype, C contiguity and room for `count` values
+            if a is None:
+                return np.zeros(count, dtype=dt)
+            if not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous or a.size < count:
+                raise ValueError(f"{name}: need a C-contiguous {np.dtype(dt).name} array of >= {count} values")
+            if not a.flags.writeable:
+                raise ValueError(f"{name}: array is read-only")
+            return a
+
+        t = out(t, np.uint32, "t")
+        x7 = out(x7, np.uint64, "x7")
+        x10 = out(x10, np.uint64, "x10")
         _check(LIB.gl_edge_counts(self._h, first, count, t.ctypes.data_as(C.c_void_p),
                                   x7.ctypes.data_as(C.c_void_p), x10.ctypes.data_as(C.c_void_p)))
         return t, x7, x10

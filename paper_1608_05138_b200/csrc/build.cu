@@ -18,11 +18,19 @@
 // the reference's loops; counts do not depend on it, so it is not built.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "graph.cuh"
 
 namespace gl {
 
 namespace {
+
+// 32-bit id-space bound (2^32 - 1); a test-only environment override lowers it
+u64 id_limit(const char* env) {
+    const char* e = std::getenv(env);
+    return e && *e ? std::strtoull(e, nullptr, 10) : 0xffffffffull;
+}
 
 constexpr int kThreads = 256;
 
@@ -252,7 +260,10 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
             sort_keys<u64>(tmp, const_cast<u64*>(d_pairs), lab_b.as<u64>(), nlab, bits_for(maxlab), s);
             n = unique_keys<u64>(tmp, lab_b.as<u64>(), lab_a.as<u64>(), nlab, cnt, s);
         }
-        if (n >= 0xffffffffull) throw overflow_error("graph exceeds 32-bit vertex id space");
+        // the reference's check and exception (graph.cpp:103-104: labels.size()
+        // >= numeric_limits<vid_t>::max() -> std::invalid_argument);
+        // GL_TEST_VERTEX_LIMIT lowers the bound so tests can reach this path
+        if (n >= id_limit("GL_TEST_VERTEX_LIMIT")) throw invalid_argument("graph exceeds 32-bit vertex id space");
         lab_b.reset();
         const u64* labels = lab_a.as<u64>();
         const int vb = bits_for(n ? n - 1 : 0);
@@ -288,7 +299,8 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
             }
             m = (nu > 0 && last == sentinel) ? nu - 1 : nu;
         }
-        if (m >= 0xffffffffull) throw overflow_error("graph exceeds 32-bit edge id space");
+        // eid_t is u32 in the reference (common.hpp:14): m < 2^32 - 1
+        if (m >= id_limit("GL_TEST_EDGE_LIMIT")) throw invalid_argument("graph exceeds 32-bit edge id space");
         keys_b.reset();
         ltab.reset();
         const u64* ekeys = keys_a.as<u64>();

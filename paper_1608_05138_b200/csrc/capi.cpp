@@ -332,7 +332,7 @@ int gl_edge_counts(const gl_graph* g, uint64_t first, uint64_t count, uint32_t* 
         auto& gr = G(g);
         const auto& cs = gr.cs;
         if (!cs.have_micro) throw gl::state_error("no counts computed yet");
-        if (first < cs.shard_begin || first + count > cs.shard_end)
+        if (first < cs.shard_begin || first > cs.shard_end || count > cs.shard_end - first)
             throw gl::invalid_argument("edge range outside the computed shard");
         GL_CUDA(cudaSetDevice(gr.device));
         // the three copies queue back to back, one synchronisation

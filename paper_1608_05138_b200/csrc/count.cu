@@ -431,6 +431,13 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     // count_mid is still writing the slot accumulators and reading the queue
     // counters: finish it before any of them is reset below.
     if (cs.s2) GL_CUDA(cudaStreamSynchronize(cs.s2));
+    // ... and the previous call's H-pass / triangle sums, which may sit on
+    // another caller stream: they pop the queue counters and write t and the
+    // partials that the memsets below reset
+    if (cs.began) {
+        GL_CUDA(cudaEventSynchronize(cs.ev[1]));
+        if (cs.mid_done) GL_CUDA(cudaEventSynchronize(cs.ev[7]));
+    }
     cs.launches = 0;
     cs.began = false;
     cs.mid_done = false;
@@ -671,6 +678,8 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     if (!s) s = gr.stream;
     CountState& cs = gr.cs;
     if (!cs.began) throw state_error("gl_count_mid before gl_count_begin");
+    // a second fold would add the slot credits to y twice
+    if (cs.mid_done) throw state_error("gl_count_mid called twice for one gl_count_begin");
     const DevGraph& g = gr.d;
     const int sms = num_sms(gr.device);
     GL_CUDA(cudaEventRecord(cs.ev[4], s));
@@ -705,7 +714,6 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     }
-    cs.work[1] = cs.work[0];
     GL_CUDA(cudaEventRecord(cs.ev[5], s));
     // join the cycle pass, then fold its per-slot C4 credits into the y rows
     // (after the sums: both update y, the fold non-atomically)
@@ -715,6 +723,7 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     }
+    GL_CUDA(cudaEventRecord(cs.ev[7], s)); // end of count_mid (re-entry fence of count_begin)
     cs.mid_done = true;
 }
 
@@ -756,6 +765,9 @@ void count_finish(Graph& gr, const i64* d_part_shard, u64 begin, u64 end, u128 C
     if (flags[0]) throw consistency_error("per-edge bound violated (x7 > C(t,2) or x10 > s_u*s_v)");
     if (flags[1]) throw overflow_error("128-bit count accumulator overflow");
     for (int i = 0; i < 17; ++i) C[i] = ((u128)h[2 * i + 1] << 64) | h[2 * i];
+    // triangle sums: one H-edge record per triangle (C3 = sum t = 3 * triangles
+    // of this shard), each an 8 B record read + 4 B t gather + 8 B RED
+    cs.work[1] = (u64)(20 * (C[3] / 3));
     cs.shard_begin = begin;
     cs.shard_end = end;
     cs.have_micro = true;
@@ -789,7 +801,7 @@ void micro_records(const Graph& gr, u64 first, u64 count, u64* host_out) {
     GL_CUDA(cudaSetDevice(gr.device));
     const CountState& cs = gr.cs;
     if (!cs.have_micro) throw state_error("no counts computed yet");
-    if (first < cs.shard_begin || first + count > cs.shard_end)
+    if (first < cs.shard_begin || first > cs.shard_end || count > cs.shard_end - first)
         throw invalid_argument("edge range outside the computed shard");
     if (count == 0) return;
     cudaStream_t s = gr.stream;

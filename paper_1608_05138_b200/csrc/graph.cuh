@@ -83,7 +83,7 @@ struct CountState {
     DevBuf keys, tmp, scratch, cursor, cursor2, acc; // sort keys, cub temp, kernel scratch
     DevBuf keys_c, items_c, tmp_c; // the cycle pass's own (it runs concurrently on s2)
     cudaStream_t s2 = nullptr;     // cycle-pass stream (owned)
-    cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork
+    cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork, 7 end of count_mid
     u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0, n_items3x = 0;
     u64 shard_begin = 0, shard_end = 0;
     bool have_micro = false;
@@ -103,6 +103,11 @@ struct Graph {
     DevBuf b_off, b_adj, b_eid, b_lcnt, b_loff, b_ev, b_eu, b_epos, b_deg, b_label;
     CountState cs;
     ~Graph() {
+        // kernels of an unfinished count may still write the buffers that go
+        // back to the (stream-unaware) pool below, on the graph's streams or a
+        // caller's: drain the device before releasing them
+        cudaSetDevice(device);
+        cudaDeviceSynchronize();
         if (cs.s2) {
             cudaStreamSynchronize(cs.s2);
             for (auto e : cs.ev)

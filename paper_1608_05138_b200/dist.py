@@ -109,6 +109,10 @@ def sharded_step(graph, partials, rank: int, world: int, stream, group=None):
     import torch
     from . import global_from_unrestricted
     dev = partials.device
+    if stream is None or stream.cuda_stream == 0:
+        # the library maps a NULL stream to the graph's own non-blocking stream,
+        # which nothing here would order against torch's collectives
+        raise ValueError("sharded_step needs a dedicated (non-default) CUDA stream")
     graph.count_begin(rank, world, partials.data_ptr(), stream.cuda_stream)
     with torch.cuda.stream(stream):
         allreduce_triangles(graph, world, group, stream=stream)
@@ -125,5 +129,9 @@ def count_sharded(graph, rank: int, world: int, group=None, stream=None):
     import torch
     dev = torch.device("cuda", graph.device)
     partials = torch.empty(2 * graph.partials_len(world), dtype=torch.int64, device=dev)
-    s = torch.cuda.current_stream(dev) if stream is None else stream
-    return sharded_step(graph, partials, rank, world, s, group)
+    cur = torch.cuda.current_stream(dev)
+    s = torch.cuda.Stream(dev) if stream is None else stream
+    s.wait_stream(cur)  # partials were allocated / zeroed on the current stream
+    out = sharded_step(graph, partials, rank, world, s, group)
+    cur.wait_stream(s)
+    return out

@@ -16,8 +16,15 @@ def pytest_configure(config):
 
 
 def golden_cases():
-    names = sorted(f[:-5] for f in os.listdir(GOLDEN) if f.endswith(".json") and f != "parser.json")
+    # small-graph goldens only: parser vectors and the full-size fixtures
+    # (full_*.json, sample_*.json from make_scale_golden.py) have their own tests
+    names = sorted(f[:-5] for f in os.listdir(GOLDEN)
+                   if f.endswith(".json") and f != "parser.json" and not f.startswith(("full_", "sample_")))
     return names
+
+
+def scale_goldens(prefix):
+    return sorted(f[:-5] for f in os.listdir(GOLDEN) if f.startswith(prefix) and f.endswith(".json"))
 
 
 def load_golden(name):

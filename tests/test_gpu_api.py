@@ -1,0 +1,79 @@
+"""GPU: boundary behaviour of the C-ABI -- the reference's error semantics,
+call-sequence errors and caller-buffer validation (no counting parity here)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+gl = pytest.importorskip("paper_1608_05138_b200")
+
+
+def test_vertex_id_space_is_invalid_argument(cuda_device, monkeypatch):
+    """graph.cpp:103-104: >= 2^32-1 distinct labels -> std::invalid_argument
+    (GL_ERR_INVALID).  GL_TEST_VERTEX_LIMIT lowers the bound to reach it."""
+    monkeypatch.setenv("GL_TEST_VERTEX_LIMIT", "4")
+    gl.Graph.build(np.array([[0, 1], [1, 2], [2, 0]], np.uint64), cuda_device)  # n = 3 < 4
+    with pytest.raises(gl.InvalidArgument, match="vertex id space"):
+        gl.Graph.build(np.array([[0, 1], [1, 2], [2, 3]], np.uint64), cuda_device)
+
+
+def test_edge_id_space_is_invalid_argument(cuda_device, monkeypatch):
+    """eid_t is u32 (common.hpp:14): m >= 2^32-1 is refused as invalid."""
+    monkeypatch.setenv("GL_TEST_EDGE_LIMIT", "3")
+    gl.Graph.build(np.array([[0, 1], [1, 2]], np.uint64), cuda_device)
+    with pytest.raises(gl.InvalidArgument, match="edge id space"):
+        gl.Graph.build(np.array([[0, 1], [1, 2], [2, 0]], np.uint64), cuda_device)
+
+
+def test_call_sequence_errors(cuda_device):
+    import torch
+    g = gl.Graph.build(gl.generate_rmat(10, 8, seed=2), cuda_device)
+    st = torch.cuda.Stream()
+    buf = torch.empty(2 * g.partials_len(1), dtype=torch.int64, device="cuda")
+    with pytest.raises(gl.StateError):
+        g.count_mid(buf.data_ptr(), st.cuda_stream)
+    g.count_begin(0, 1, buf.data_ptr(), st.cuda_stream)
+    g.count_mid(buf.data_ptr(), st.cuda_stream)
+    with pytest.raises(gl.StateError, match="twice"):
+        g.count_mid(buf.data_ptr(), st.cuda_stream)
+    C = g.count_finish(buf.data_ptr(), 0, g.num_edges(), st.cuda_stream)
+    assert gl.global_from_unrestricted(C, g.num_vertices(), g.num_edges()) == g.count().X
+    # re-entry: begin twice on different streams before mid gives the same counts
+    st2 = torch.cuda.Stream()
+    g.count_begin(0, 1, buf.data_ptr(), st.cuda_stream)
+    g.count_begin(0, 1, buf.data_ptr(), st2.cuda_stream)
+    g.count_mid(buf.data_ptr(), st2.cuda_stream)
+    C2 = g.count_finish(buf.data_ptr(), 0, g.num_edges(), st2.cuda_stream)
+    assert C2 == C
+
+
+def test_edge_counts_validates_caller_buffers(cuda_device):
+    g = gl.Graph.build(gl.generate_rmat(9, 8, seed=4), cuda_device)
+    g.count()
+    m = g.num_edges()
+    t, x7, x10 = g.edge_counts()
+    with pytest.raises(ValueError):
+        g.edge_counts(0, m, t=np.zeros(m, np.int64))  # wrong dtype
+    with pytest.raises(ValueError):
+        g.edge_counts(0, m, x7=np.zeros(m - 1, np.uint64))  # too short
+    with pytest.raises(ValueError):
+        g.edge_counts(0, m, x10=np.zeros(2 * m, np.uint64)[::2])  # not contiguous
+    # first + count wraps around 2^64: refused by the C range check itself
+    assert gl.LIB.gl_edge_counts(g._h, 5, 2**64 - 3, None, None, None) == -1
+    t2, a, b = g.edge_counts(0, m, t=np.zeros(m + 5, np.uint32))
+    assert np.array_equal(t2[:m], t)
+    rec = np.zeros(m, gl.MICRO_DTYPE)
+    assert np.array_equal(g.micro_records(out=rec), g.micro_records())
+
+
+def test_count_sharded_world1_on_default_stream(cuda_device):
+    """dist.count_sharded without a stream runs on its own stream ordered after
+    the caller's (never the library's unordered NULL-stream mapping)."""
+    from paper_1608_05138_b200.dist import count_sharded, sharded_step
+    import torch
+    g = gl.Graph.build(gl.generate_rmat(11, 16, seed=9), cuda_device)
+    X, (b, e) = count_sharded(g, 0, 1)
+    assert X == g.count().X and (b, e) == (0, g.num_edges())
+    p = torch.empty(2 * g.partials_len(1), dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError, match="stream"):
+        sharded_step(g, p, 0, 1, torch.cuda.default_stream())

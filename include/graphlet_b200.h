@@ -181,6 +181,14 @@ int gl_last_timings(const gl_graph *g, float ms[5], uint32_t *launches);
 /* Algorithmic work counters of the last count call:
  * algorithmic bytes per phase, same order as gl_last_timings [0..3]. */
 int gl_last_work(const gl_graph *g, uint64_t work[4]);
+/* Work items of the cycle pass's windowed (heavy) tops in the last
+ * gl_count_begin, all ranks: 4 x u32 per item = (top a, c_lo, c_hi, wedge
+ * estimate); item i covers the wedges a-b-c with c in [c_lo, c_hi).  A top
+ * above the piece cap is split into several such c-range pieces, the unit of
+ * fine-grained task splitting (reference cycle_res_range + split_threshold,
+ * include/graphlet/kernels.hpp:68-80).  Writes min(*count_total, cap) items;
+ * out may be NULL to query the count. */
+int gl_cycle_pieces(const gl_graph *g, uint32_t *out, uint64_t cap, uint64_t *count_total);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,7 @@ _sig("gl_edge_counts_device", C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.POIN
      C.POINTER(C.c_void_p))
 _sig("gl_last_timings", C.c_int, C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_uint32))
 _sig("gl_last_work", C.c_int, C.c_void_p, _u64p)
+_sig("gl_cycle_pieces", C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, _u64p)
 
 
 class GraphletError(RuntimeError):
@@ -355,6 +356,15 @@ class Graph:
         w = (C.c_uint64 * 4)()
         _check(LIB.gl_last_work(self._h, w))
         return [float(x) for x in ms], int(nl.value), [int(x) for x in w]
+
+    def cycle_pieces(self) -> np.ndarray:
+        """Windowed-top work items of the last count: rows (a, c_lo, c_hi, wedge estimate)."""
+        n = C.c_uint64()
+        _check(LIB.gl_cycle_pieces(self._h, None, 0, C.byref(n)))
+        out = np.zeros((n.value, 4), dtype=np.uint32)
+        if n.value:
+            _check(LIB.gl_cycle_pieces(self._h, out.ctypes.data_as(C.c_void_p), n.value, C.byref(n)))
+        return out
 
     # sharded (one process per GPU) form -------------------------------------
     def partials_len(self, world: int) -> int:

@@ -374,4 +374,19 @@ int gl_last_work(const gl_graph* g, uint64_t work[4]) {
     });
 }
 
+int gl_cycle_pieces(const gl_graph* g, uint32_t* out, uint64_t cap, uint64_t* count_total) {
+    return guarded([&] {
+        auto& gr = G(g);
+        if (!gr.cs.began) throw gl::state_error("no gl_count_begin yet");
+        const uint64_t n = gr.cs.cycle_pieces;
+        if (count_total) *count_total = n;
+        const uint64_t k = n < cap ? n : cap;
+        if (!out || !k) return;
+        GL_CUDA(cudaSetDevice(gr.device));
+        if (gr.cs.s2) GL_CUDA(cudaStreamSynchronize(gr.cs.s2));
+        GL_CUDA(cudaStreamSynchronize(gr.stream));
+        GL_CUDA(cudaMemcpy(out, gr.cs.pieces.p, k * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    });
+}
+
 } // extern "C"

@@ -345,13 +345,87 @@ __global__ void k_tiers(DevGraph g, unsigned* __restrict__ out) {
 constexpr int kCounters = 32;
 
 // rank's share of a cost-sorted list: sorted positions p with p % world == rank
-__global__ void k_take_rank(const u32* __restrict__ sorted, u64 begin, u64 count, int rank, int world,
-                            u32* __restrict__ out) {
+template <typename T>
+__global__ void k_take_rank(const T* __restrict__ sorted, u64 begin, u64 count, int rank, int world,
+                            T* __restrict__ out) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;; i += (u64)gridDim.x * blockDim.x) {
         u64 p = (u64)rank + i * (u64)world;
         if (p >= count) break;
         out[i] = sorted[begin + p];
     }
+}
+
+// ------------------------------------------------------ heavy-top pieces
+// A windowed top (dense or sparse big) whose wedges exceed the piece cap is
+// split into c-range pieces [clo, chi) of about equal wedge count: the unit of
+// fine-grained task splitting (the reference's clique_res_range /
+// cycle_res_range with split_threshold, kernels.hpp:68-80), so no
+// single block or rank holds more than ~1/4096 of the cycle work.  Pieces are
+// laid out in sorted-top order (deterministic: every rank derives the same
+// list and takes its positions p % world).
+constexpr u32 kPieceSamples = 2048; // sampled wedges per split top (256 threads x 8)
+constexpr u32 kPieceMax = kPieceSamples / 4;
+__device__ __forceinline__ u32 piece_count(const DevGraph& g, const u64* __restrict__ wpre, u32 a, u64 cap) {
+    const u64 E0 = g.loff[a], E1 = g.loff[a + 1];
+    const u64 w = wpre[E1] - wpre[E0], nb = E1 - E0;
+    u64 p = (w + cap - 1) / cap;
+    // every piece re-seeks each b's cursor (one binary search per b): keep
+    // >= 32 wedges per b per piece
+    const u64 pb = nb ? w / (32 * nb) : 1;
+    p = p < pb ? p : pb;
+    p = p < kPieceMax ? p : kPieceMax;
+    return p ? (u32)p : 1u;
+}
+__global__ void k_piece_count(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ sorted, u64 count,
+                              u64 cap, u32* __restrict__ np) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x)
+        np[i] = piece_count(g, wpre, sorted[i], cap);
+}
+// one block per windowed top: c quantiles of kPieceSamples evenly spaced
+// wedges (wedge order is b-major, so the samples are not c-ordered: sort them)
+__global__ void __launch_bounds__(256) k_pieces(DevGraph g, const u64* __restrict__ wpre,
+                                                const u32* __restrict__ sorted, u64 count,
+                                                const u32* __restrict__ poff, uint4* __restrict__ pieces) {
+    using Sort = cub::BlockRadixSort<u32, 256, kPieceSamples / 256>;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ u32 s_c[kPieceSamples];
+    for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
+        const u32 a = sorted[i];
+        const u32 P = poff[i + 1] - poff[i];
+        const u64 E0 = g.loff[a], E1 = g.loff[a + 1];
+        const u64 w0 = wpre[E0], w = wpre[E1] - w0;
+        uint4* out = pieces + poff[i];
+        if (P == 1) {
+            if (threadIdx.x == 0) out[0] = make_uint4(a, 0u, a, (u32)min(w, (u64)0xffffffffull));
+            continue;
+        }
+        u32 keys[kPieceSamples / 256];
+#pragma unroll
+        for (u32 u = 0; u < kPieceSamples / 256; ++u) {
+            const u64 sidx = threadIdx.x * (kPieceSamples / 256) + u;
+            const u64 k = w0 + (2 * sidx + 1) * w / (2 * kPieceSamples);
+            const u64 e = upper_bound_dev<u64, u64>(wpre, E0, E1 + 1, k) - 1;
+            keys[u] = g.adj[g.off[g.eu[e]] + (k - wpre[e])];
+        }
+        __syncthreads(); // tmp / s_c reuse across tops
+        Sort(tmp).Sort(keys);
+#pragma unroll
+        for (u32 u = 0; u < kPieceSamples / 256; ++u) s_c[threadIdx.x * (kPieceSamples / 256) + u] = keys[u];
+        __syncthreads();
+        const u32 west = (u32)min((w + P - 1) / P, (u64)0xffffffffull);
+        for (u32 j = threadIdx.x; j < P; j += blockDim.x) {
+            const u32 lo = j ? s_c[(u64)j * kPieceSamples / P] : 0u;
+            const u32 hi = j + 1 < P ? s_c[(u64)(j + 1) * kPieceSamples / P] : a;
+            out[j] = make_uint4(a, lo, hi, west);
+        }
+    }
+}
+// piece cap: total wedges / 4096 (at least 2^17); GL_PIECE_WEDGES=<n> overrides
+// (tests force splitting on small graphs)
+inline u64 piece_cap(u64 wtot) {
+    if (const char* e = std::getenv("GL_PIECE_WEDGES"))
+        if (*e >= '0' && *e <= '9') return std::max<u64>(1, std::strtoull(e, nullptr, 10));
+    return std::max<u64>(wtot / 4096, 1ull << 17);
 }
 
 struct Timer {
@@ -466,7 +540,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     }
     cudaStream_t s2 = g_overlap.load() ? cs.s2 : s; // serial mode: everything on s
     cs.keys_c.alloc((n + 1) * 2 * sizeof(u32));
-    cs.items_c.alloc((n + 1) * 2 * sizeof(u32));
+    cs.items_c.alloc((n + 1) * 3 * sizeof(u32)); // id in/out, piece offsets
     GL_CUDA(cudaEventRecord(cs.ev[0], s));
     if (m == 0) {
         for (int i = 1; i < 4; ++i) GL_CUDA(cudaEventRecord(cs.ev[i], s));
@@ -550,7 +624,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 auto launch = [&](auto kc, u64 count, u64 offset, u64 total, u32* list, u64 hbase, u64 hcap,
                                   unsigned long long* queue) {
                     constexpr int K = decltype(kc)::value;
-                    k_take_rank<<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
+                    k_take_rank<u32><<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
                     const u32 kws = K == 1088 ? 1088u : (K == 768 ? 512u : 128u); // largest k of the class
                     const size_t smem =
@@ -576,7 +650,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                            myxl + mybig, hcap_m, counters + 8);
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nxl + nbig + nmedk, nsmall, rank, world,
+                k_take_rank<u32><<<grid1d(mysmall, 256, sms), 256, 0, s>>>(iout, nxl + nbig + nmedk, nsmall, rank, world,
                                                                       cs.items3s.as<u32>());
                 GL_LAUNCH_CHECK();
                 const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20,
@@ -619,12 +693,43 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             const u64 mymid = rank_share(nmid, rank, world);
             const u64 mysmid = rank_share(nsmid, rank, world);
             const u64 mysmall = rank_share(nsmall, rank, world);
+            // windowed tops -> pieces (positions [0, nsparse + nbig) of the sorted list)
+            const u64 nwin = nsparse + nbig;
+            u64 psparse = 0, pbig = 0;
+            if (nwin) {
+                u32* np = kin; // scratch: keys are sorted into kout already
+                k_piece_count<<<grid1d(nwin, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), iout, nwin, piece_cap(wtot),
+                                                                    np);
+                GL_CUDA(cudaMemsetAsync(np + nwin, 0, sizeof(u32), s2));
+                u32* poff = cs.items_c.as<u32>() + 2 * (n + 1); // see the allocation above
+                dev_exclusive_scan<u32>(cs.tmp_c, np, poff, nwin + 1, s2);
+                u32 hp[2];
+                GL_CUDA(cudaMemcpyAsync(&hp[0], poff + nsparse, sizeof(u32), cudaMemcpyDeviceToHost, s2));
+                GL_CUDA(cudaMemcpyAsync(&hp[1], poff + nwin, sizeof(u32), cudaMemcpyDeviceToHost, s2));
+                GL_CUDA(cudaStreamSynchronize(s2));
+                psparse = hp[0];
+                pbig = hp[1] - hp[0];
+                cs.pieces.alloc(((u64)hp[1] * 2 + 2) * sizeof(uint4)); // all pieces, then this rank's share
+                k_pieces<<<(unsigned)std::min<u64>(nwin, (u64)sms * 8), 256, 0, s2>>>(g, cs.wpre.as<u64>(), iout, nwin,
+                                                                                  poff, cs.pieces.as<uint4>());
+                GL_LAUNCH_CHECK();
+                cs.launches += 4;
+                if (std::getenv("GL_DEBUG"))
+                    std::fprintf(stderr, "[gl] cycle pieces: %llu sparse-big, %llu big (from %llu windowed tops, cap %llu)\n",
+                                 (unsigned long long)psparse, (unsigned long long)pbig, (unsigned long long)nwin,
+                                 (unsigned long long)piece_cap(wtot));
+            }
+            const u64 mysparse_p = rank_share(psparse, rank, world), mybig_p = rank_share(pbig, rank, world);
+            uint4* pall = cs.pieces.as<uint4>();
+            uint4* psp = pall + psparse + pbig;
+            uint4* pbg = psp + mysparse_p;
+            cs.cycle_pieces = psparse + pbig;
             u32* lsparse = iin;
             u32* lbig = lsparse + mysparse;
             u32* lmid = lbig + mybig;
             u32* lsmid = lmid + mymid;
             u32* lsmall = lsmid + mysmid;
-            if (mysparse || mybig || mymid || mysmid) {
+            if (mysparse_p || mybig_p || mymid || mysmid) {
                 if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
                 // per-block scratch: big tops need dmax + 2 entries, hash tops at most
                 // their wedge bound (nb <= wedges)
@@ -632,30 +737,38 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const u32 cap_hash = std::min<u32>(cap_big, (u32)kMidWedges + 2);
                 const u64 w_big = (big_scratch_words(cap_big) + 1) & ~1ull;
                 const u64 w_hash = (big_scratch_words(cap_hash) + 1) & ~1ull;
-                if (mybig || mysparse) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
+                if (mybig_p || mysparse_p) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
                 if (mymid || mysmid) cs.cursor2.alloc((u64)sms * 4 * w_hash * sizeof(u32));
                 auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
                     constexpr int K = decltype(kind)::value;
+                    constexpr bool WIN = Cyc<K>::WIN;
                     const u32 cap = K == 0 || K == 3 ? cap_big : cap_hash;
                     u32* scratch = K == 0 || K == 3 ? cs.cursor.as<u32>() : cs.cursor2.as<u32>();
-                    k_take_rank<<<grid1d(count, 256, sms), 256, 0, s2>>>(iout, offset, total, rank, world, list);
+                    uint4* plist = K == 3 ? psp : pbg;
+                    if (WIN)
+                        k_take_rank<uint4><<<grid1d(count, 256, sms), 256, 0, s2>>>(pall, offset, total, rank, world,
+                                                                                    plist);
+                    else
+                        k_take_rank<u32><<<grid1d(count, 256, sms), 256, 0, s2>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
                     smem_attr(k_cycle_block<K>, smem, gr.device);
                     k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s2>>>(
-                        g, list, count, queue, cs.slots.as<i64>(), scratch, cap, tiers);
+                        g, list, plist, count, queue, cs.slots.as<i64>(), scratch, cap, tiers);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };
-                // sorted list: [sparse big | big | mid | small-mid | small]
-                if (mysparse) launch(std::integral_constant<int, 3>{}, lsparse, mysparse, 0, nsparse, counters + 28);
-                if (mybig) launch(std::integral_constant<int, 0>{}, lbig, mybig, nsparse, nbig, counters + 1);
+                // sorted list: [sparse big | big | mid | small-mid | small]; the
+                // windowed classes go as pieces [sparse big pieces | big pieces]
+                if (mysparse_p)
+                    launch(std::integral_constant<int, 3>{}, nullptr, mysparse_p, 0, psparse, counters + 28);
+                if (mybig_p) launch(std::integral_constant<int, 0>{}, nullptr, mybig_p, psparse, pbig, counters + 1);
                 if (mymid) launch(std::integral_constant<int, 1>{}, lmid, mymid, nsparse + nbig, nmid, counters + 4);
                 if (mysmid)
                     launch(std::integral_constant<int, 2>{}, lsmid, mysmid, nsparse + nbig + nmid, nsmid, counters + 7);
             }
             if (mysmall) {
-                k_take_rank<<<grid1d(mysmall, 256, sms), 256, 0, s2>>>(iout, nsparse + nbig + nmid + nsmid, nsmall, rank,
+                k_take_rank<u32><<<grid1d(mysmall, 256, sms), 256, 0, s2>>>(iout, nsparse + nbig + nmid + nsmid, nsmall, rank,
                                                                        world, lsmall);
                 GL_LAUNCH_CHECK();
                 const size_t smem = (size_t)kCycleSmallWarps * kSmallWarpWords * sizeof(u32);

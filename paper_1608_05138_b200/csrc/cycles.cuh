@@ -544,13 +544,14 @@ __device__ __forceinline__ void meta_pass(const DevGraph& g, const RunMeta& Msm,
 
 template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
-k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
-              i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap, uint4 tiers) {
+k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict__ pieces, u64 n_items,
+              unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap,
+              uint4 tiers) {
     constexpr bool HASH = Cyc<KIND>::HASH, WIN = Cyc<KIND>::WIN;
     constexpr int THREADS = Cyc<KIND>::THREADS;
     constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
     extern __shared__ u32 W[]; // kWords table words, then the run metadata
-    __shared__ unsigned long long s_idx, s_rem;
+    __shared__ unsigned long long s_idx;
     __shared__ u32 s_next, s_work[3];
     BigScratch S = big_scratch(gscratch + (u64)blockIdx.x * ((big_scratch_words(cap) + 1) & ~1ull), cap);
     const RunMeta Msm{W + kWords, W + kWords + kMeta + 1, W + kWords + 2 * kMeta + 1};
@@ -585,7 +586,14 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const unsigned long long idx = s_idx;
         if (idx >= n_items) break;
         GL_PROF_MARK(5);
-        const u32 a = items[idx];
+        // windowed kinds take pieces (a, clo, chi, wedge estimate): the wedges
+        // of top a whose c lies in [clo, chi) -- a heavy top is split into
+        // c-range pieces that different blocks (and ranks) take; every credit is
+        // an atomic add, so the pieces of a top sum exactly
+        uint4 pc = make_uint4(0, 0, 0, 0);
+        if constexpr (WIN) pc = pieces[idx];
+        const u32 a = WIN ? pc.x : items[idx];
+        const u32 clo = pc.y, chi = WIN ? pc.z : a;
         const u64 E0 = g.loff[a];
         const u32 nb = (u32)(g.loff[a + 1] - E0);
         const u64 abase = g.off[a]; // slot of (a, b_j) is abase + j: L(a) is the row prefix
@@ -638,52 +646,51 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             GL_PROF_SYNC_MARK(7);
             continue;
         }
-        if (threadIdx.x == 0) {
-            s_next = WIN ? kEmpty : 0u;
-            s_rem = 0;
-        }
+        if (threadIdx.x == 0) s_next = WIN ? kEmpty : 0u;
         __syncthreads();
-        u64 my_rem = 0;
-        // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at 0
+        // per-b row base and run end (|N(b) n [0,a)| = epos), cursors at the
+        // piece's first c (0 for an unsplit top or a first piece); the piece's
+        // upper end chi is a window boundary, found by the window loop's run search
         for (u32 j = threadIdx.x; j < nb; j += THREADS) {
             const u64 e = E0 + j;
             const u64 rb = g.off[g.eu[e]];
             const u32 re = g.epos[e];
             S.rb[j] = rb;
             S.rend[j] = re;
-            S.cur[j] = 0;
-            const u32 c = re > 0 ? g.adj[rb] : kEmpty;
+            u32 c0 = 0;
+            if (clo && re) c0 = g.adj[rb + re - 1] < clo ? re : (u32)(lower_bound_dev<u32, u64>(g.adj, rb, rb + re, clo) - rb);
+            S.cur[j] = c0;
+            const u32 c = c0 < re ? g.adj[rb + c0] : kEmpty;
             if (WIN) S.lastc[j] = re > 0 ? g.adj[rb + re - 1] : 0u;
-            S.nextc[j] = c;
+            S.nextc[j] = c < chi ? c : kEmpty;
             S.rwin[j] = kEmpty;
             S.plen[j] = 0;
-            if (WIN && c != kEmpty) atomicMin(&s_next, c);
-            my_rem += re;
+            if (WIN && c < chi) atomicMin(&s_next, c);
         }
-        if (KIND == 3 && my_rem) atomicAdd(&s_rem, (unsigned long long)my_rem);
         __syncthreads();
-        u64 rem = s_rem; // wedges of this top not yet in a window (KIND 3 window sizing)
+        u64 rem = pc.w; // wedges of this piece not yet in a window (KIND 3 window sizing; estimate for a split top)
         GL_PROF_MARK(0);
         GL_PROF_ADD(10, 1);
         // Windows from the smallest c on.  Each b keeps its cursor and the c
         // value under it (nextc), so a window only gallops the b's whose next c
         // falls inside it; for the others one coalesced nextc load suffices.
         u32 win = 0;
-        for (u32 lo = s_next, hi = 0; lo < a; lo = hi, ++win) {
+        for (u32 lo = s_next, hi = 0; lo < chi; lo = hi, ++win) {
             // window [lo, hi): inside one degree tier, counters of that tier's width
-            u32 cl = 1, tend = a;
+            u32 cl = 1, tend = chi;
             if (!HASH) {
                 cl = lo < tiers.x ? 4u : lo < tiers.y ? 3u : lo < tiers.z ? 2u : lo < tiers.w ? 1u : 0u;
-                tend = lo < tiers.x ? tiers.x : lo < tiers.y ? tiers.y : lo < tiers.z ? tiers.z : lo < tiers.w ? tiers.w : a;
+                tend = lo < tiers.x ? tiers.x : lo < tiers.y ? tiers.y : lo < tiers.z ? tiers.z : lo < tiers.w ? tiers.w : chi;
+                tend = tend < chi ? tend : chi;
             }
             u64 span = (u64)kWindow << cl;
-            if (KIND == 3) { // about kHashWinTarget wedges if they were uniform over [lo, a)
-                span = rem ? (u64)(a - lo) * kHashWinTarget / rem : (u64)(a - lo);
+            if (KIND == 3) { // about kHashWinTarget wedges if they were uniform over [lo, chi)
+                span = rem ? (u64)(chi - lo) * kHashWinTarget / rem : (u64)(chi - lo);
                 span = span ? span : 1;
             }
             // keep nb * span < 2^31: window wedge counts and indices are u32
             if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
-            hi = !WIN ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)a);
+            hi = !WIN ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)chi);
 
             u32 my_runs, my_wedges, nnz, T;
             u64 mine;
@@ -751,7 +758,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                     break;
                 }
             }
-            rem -= T;
+            rem = rem > T ? rem - T : 0;
 #ifdef GL_CYCLE_PROF
             if (KIND == 3 && threadIdx.x == 0) {
                 atomicAdd(&g_cycle_prof[30], 1ull);

@@ -82,6 +82,8 @@ struct CountState {
     DevBuf items2, items3s, items3m, items3b, items3x; // work lists
     DevBuf keys, tmp, scratch, cursor, cursor2, acc; // sort keys, cub temp, kernel scratch
     DevBuf keys_c, items_c, tmp_c; // the cycle pass's own (it runs concurrently on s2)
+    DevBuf pieces;                 // uint4 (a, clo, chi, wedge estimate): windowed-top pieces, then the rank's share
+    u64 cycle_pieces = 0;
     cudaStream_t s2 = nullptr;     // cycle-pass stream (owned)
     cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork, 7 end of count_mid
     u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0, n_items3x = 0;

@@ -238,14 +238,78 @@ def test_hub_full_counters(cuda_device):
     assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
 
 
-@pytest.mark.parametrize("graph,sparse,world", [("rmat12", None, 2), ("ba60k", None, 2), ("ba60k", "off", 2), ("ba60k", "all", 2), ("ba60k", "all", 3)])
-def test_sharded_equals_single(cuda_device, monkeypatch, graph, sparse, world):
+def _piece_wedges(g, pieces):
+    """Exact wedges a-b-c (b in L(a), c in N(b), c < a) with c in [lo, hi) of
+    every piece row (a, lo, hi, est), from the CSR on the host."""
+    off, adj = g.csr()
+    off = off.astype(np.int64)
+    n = g.num_vertices()
+    row = np.repeat(np.arange(n, dtype=np.int64), np.diff(off))
+    key = row * n + adj.astype(np.int64)  # ascending: rows by id, each row ascending
+    out = np.zeros(len(pieces), np.int64)
+    for i, (a, lo, hi, _) in enumerate(pieces.astype(np.int64)):
+        r = adj[off[a]:off[a + 1]].astype(np.int64)
+        b = r[r < a]
+        hi = min(hi, a)
+        if hi > lo and len(b):
+            out[i] = int((np.searchsorted(key, b * n + hi) - np.searchsorted(key, b * n + lo)).sum())
+    return out
+
+
+@pytest.mark.parametrize("graph,cap,sparse", [("ba60k", 3000, None), ("ba60k", 3000, "all"), ("ba200k", 4000, None),
+                                              ("rmat13", 2000, None), ("rmat13", 2000, "all"), ("hub", 50000, None)])
+def test_cycle_pieces(cuda_device, monkeypatch, graph, cap, sparse):
+    """Heavy windowed tops split into c-range pieces (GL_PIECE_WEDGES forces a
+    small piece cap): counts stay bit-exact, the pieces of each top tile
+    [0, a) without gaps or overlap, and a split top's pieces share its wedges."""
+    monkeypatch.setenv("GL_PIECE_WEDGES", str(cap))
+    if sparse:
+        monkeypatch.setenv("GL_SPARSE_BIG", sparse)
+    if graph == "hub":
+        rng = np.random.default_rng(7)
+        leaves = 70000
+        hub = [(0, i) for i in range(1, leaves + 1)]
+        hub2 = [(leaves + 1, int(i)) for i in rng.choice(np.arange(1, leaves + 1), 3000, replace=False)]
+        ab = rng.integers(1, leaves + 1, size=(20000, 2))
+        pairs = np.array(hub + hub2 + [tuple(map(int, r)) for r in ab], dtype=np.uint64)
+    elif graph == "rmat13":
+        pairs = gl.generate_rmat(13, 16, seed=13)
+    else:
+        n, k, seed = (60000, 6, 3) if graph == "ba60k" else (200000, 4, 11)
+        pairs = gl.generate_ba(n, k, seed=seed)
+    o = Oracle(pairs)
+    X, orec = o.count(threads=THREADS, micro=True)
+    g, res, rec = gpu_count(pairs, cuda_device)
+    assert res.X == X
+    assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+    P = g.cycle_pieces()
+    tops, counts = np.unique(P[:, 0], return_counts=True)
+    assert counts.max() > 1, "no top was split"
+    for a in tops[counts > 1]:
+        rows = P[P[:, 0] == a]
+        rows = rows[np.argsort(rows[:, 1], kind="stable")]
+        assert rows[0, 1] == 0 and rows[-1, 2] == a
+        assert np.array_equal(rows[1:, 1], rows[:-1, 2])  # contiguous tiling of [0, a)
+    w = _piece_wedges(g, P)
+    split = np.isin(P[:, 0], tops[counts > 1])
+    # quantile cuts from 2048 sampled wedges: a split top's pieces stay near the cap
+    assert w[split].max() <= 3 * max(cap, int(P[split, 3].max()))
+
+
+@pytest.mark.parametrize("graph,sparse,world,piece", [("rmat12", None, 2, None), ("ba60k", None, 2, None),
+                                                      ("ba60k", "off", 2, None), ("ba60k", "all", 2, None),
+                                                      ("ba60k", "all", 3, None), ("ba60k", None, 3, 2000),
+                                                      ("rmat12", "all", 2, 1500)])
+def test_sharded_equals_single(cuda_device, monkeypatch, graph, sparse, world, piece):
     """world=2/3 sharding emulated on one GPU: begin per rank, sum partial rows,
     finish per shard, sum unrestricted -> identical macro and micro (BA 60k
-    with GL_SPARSE_BIG=all: the windowed-hash tops are split across ranks)."""
+    with GL_SPARSE_BIG=all: the windowed-hash tops are split across ranks;
+    with a piece cap: the c-range pieces of one top land on different ranks)."""
     import torch
     if sparse:
         monkeypatch.setenv("GL_SPARSE_BIG", sparse)
+    if piece:
+        monkeypatch.setenv("GL_PIECE_WEDGES", str(piece))
     pairs = gl.generate_rmat(12, 16, seed=5) if graph == "rmat12" else gl.generate_ba(60000, 6, seed=3)
     g = gl.Graph.build(pairs, cuda_device)
     full = g.count()

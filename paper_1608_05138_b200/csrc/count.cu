@@ -260,7 +260,7 @@ __device__ __forceinline__ u64 dense_windows(u32 a, const unsigned* __restrict__
     u32 prev = 0;
     for (int i = 0; i <= 4; ++i) {
         const u32 end = i < 4 ? (tiers[i] < a ? tiers[i] : a) : a;
-        const u64 span = (u64)kWindow << (4 - i);
+        const u64 span = (u64)(4 - i >= (int)kWalkCl ? (kWindow + 3 * 7168) & ~3 : kWindow) << (4 - i); // kWalkWords for walk tiers
         if (end > prev) nw += (end - prev + span - 1) / span;
         prev = end > prev ? end : prev;
     }
@@ -365,27 +365,33 @@ __global__ void k_take_rank(const T* __restrict__ sorted, u64 begin, u64 count, 
 // list and takes its positions p % world).
 constexpr u32 kPieceSamples = 2048; // sampled wedges per split top (256 threads x 8)
 constexpr u32 kPieceMax = kPieceSamples / 4;
-__device__ __forceinline__ u32 piece_count(const DevGraph& g, const u64* __restrict__ wpre, u32 a, u64 cap) {
+__device__ __forceinline__ u32 piece_count(const DevGraph& g, const u64* __restrict__ wpre, u32 a, u64 cap,
+                                           u32 min_per_b) {
     const u64 E0 = g.loff[a], E1 = g.loff[a + 1];
     const u64 w = wpre[E1] - wpre[E0], nb = E1 - E0;
     u64 p = (w + cap - 1) / cap;
-    // every piece re-seeks each b's cursor (one binary search per b): keep
-    // >= 32 wedges per b per piece
-    const u64 pb = nb ? w / (32 * nb) : 1;
+    // every piece re-seeks each b's cursor (a gallop per b): keep >= min_per_b
+    // (32) wedges per b per piece
+    const u64 pb = nb ? w / (min_per_b * nb) : 1;
     p = p < pb ? p : pb;
     p = p < kPieceMax ? p : kPieceMax;
     return p ? (u32)p : 1u;
 }
 __global__ void k_piece_count(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ sorted, u64 count,
-                              u64 cap, u32* __restrict__ np) {
+                              u64 cap, u32 min_per_b, u32* __restrict__ np) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x)
-        np[i] = piece_count(g, wpre, sorted[i], cap);
+        np[i] = piece_count(g, wpre, sorted[i], cap, min_per_b);
 }
 // one block per windowed top: c quantiles of kPieceSamples evenly spaced
 // wedges (wedge order is b-major, so the samples are not c-ordered: sort them)
+// Dense tops (positions >= n_hash) cut on their window grid: the pieces hold
+// exactly the unsplit top's windows (no extra window or run); cut points that
+// coincide leave empty pieces (a = kEmpty, skipped by the kernel).
 __global__ void __launch_bounds__(256) k_pieces(DevGraph g, const u64* __restrict__ wpre,
-                                                const u32* __restrict__ sorted, u64 count,
+                                                const u32* __restrict__ sorted, u64 count, u64 n_hash,
+                                                const unsigned* __restrict__ tiers_in, u32 walk_cl,
                                                 const u32* __restrict__ poff, uint4* __restrict__ pieces) {
+    const uint4 tiers = make_uint4(tiers_in[0], tiers_in[1], tiers_in[2], tiers_in[3]);
     using Sort = cub::BlockRadixSort<u32, 256, kPieceSamples / 256>;
     __shared__ typename Sort::TempStorage tmp;
     __shared__ u32 s_c[kPieceSamples];
@@ -413,19 +419,66 @@ __global__ void __launch_bounds__(256) k_pieces(DevGraph g, const u64* __restric
         for (u32 u = 0; u < kPieceSamples / 256; ++u) s_c[threadIdx.x * (kPieceSamples / 256) + u] = keys[u];
         __syncthreads();
         const u32 west = (u32)min((w + P - 1) / P, (u64)0xffffffffull);
+        const bool dense = i >= n_hash;
+        auto cut = [&](u32 j) -> u32 { // cut point j (0 < j < P)
+            const u32 c = s_c[(u64)j * kPieceSamples / P];
+            return dense ? grid_floor(c, tiers, E1 - E0, walk_cl) : c;
+        };
         for (u32 j = threadIdx.x; j < P; j += blockDim.x) {
-            const u32 lo = j ? s_c[(u64)j * kPieceSamples / P] : 0u;
-            const u32 hi = j + 1 < P ? s_c[(u64)(j + 1) * kPieceSamples / P] : a;
-            out[j] = make_uint4(a, lo, hi, west);
+            const u32 lo = j ? cut(j) : 0u;
+            const u32 hi = j + 1 < P ? cut(j + 1) : a;
+            out[j] = lo < hi ? make_uint4(a, lo, hi, west) : make_uint4(kEmpty, 0u, 0u, 0u);
         }
     }
 }
-// piece cap: total wedges / 4096 (at least 2^17); GL_PIECE_WEDGES=<n> overrides
-// (tests force splitting on small graphs)
-inline u64 piece_cap(u64 wtot) {
-    if (const char* e = std::getenv("GL_PIECE_WEDGES"))
-        if (*e >= '0' && *e <= '9') return std::max<u64>(1, std::strtoull(e, nullptr, 10));
-    return std::max<u64>(wtot / 4096, 1ull << 17);
+// ------------------------------------------------------- run-end table
+// Dense windows lie on a global grid (degree tiers cut into windows of the
+// tier's span, cycles.cuh win_span): the window of an id c is a function of c
+// alone, so the run of row b inside any window ends at the first slot after
+// the run start whose c lies in a later window.  One table per graph (and
+// walk_cl): flag every slot that starts a row or changes window, then a
+// forward min-scan over the slots in reverse order gives, for every slot p,
+// the first flagged slot >= p -- read at p + 1 it is p's run end.
+//   rev[i] = (slot 2m-1-i flagged) ? 2m-1-i : kEmpty;   table = min-scan(rev)
+//   run end after slot p = table[2m - 2 - p]  (kEmpty: none -> row prefix end)
+__device__ __forceinline__ u64 grid_win(u32 c, uint4 tiers, u32 walk_cl) {
+    u32 t0, t1;
+    const u32 cl = tier_of(c, tiers, t0, t1);
+    return ((u64)(4 - cl) << 40) | ((c - t0) / win_span(cl, 0, walk_cl));
+}
+__global__ void k_run_flags(DevGraph g, uint4 tiers, u32 walk_cl, u32* __restrict__ rev) {
+    const u64 S = 2 * g.m;
+    for (u64 p = blockIdx.x * (u64)blockDim.x + threadIdx.x; p < S; p += (u64)gridDim.x * blockDim.x) {
+        const bool f = p == 0 || grid_win(g.adj[p], tiers, walk_cl) != grid_win(g.adj[p - 1], tiers, walk_cl);
+        rev[S - 1 - p] = f ? (u32)p : kEmpty;
+    }
+}
+__global__ void k_row_flags(DevGraph g, u32* __restrict__ rev) {
+    const u64 S = 2 * g.m;
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < g.n; v += (u64)gridDim.x * blockDim.x) {
+        const u64 p = g.off[v];
+        if (p < g.off[v + 1]) rev[S - 1 - p] = (u32)p;
+    }
+}
+struct MinU32 {
+    __device__ __forceinline__ u32 operator()(u32 a, u32 b) const { return a < b ? a : b; }
+};
+
+// Piece cap: no work item above 1/4 of one SM's fair share of the job,
+// wedges / (4 * SMs * ranks) (at least 2^17): 1/592 of the cycle work on one
+// B200, 1/4736 at 8 ranks.  GL_PIECE_WEDGES=<n> overrides it (and lowers the
+// wedges-per-b floor to 1), so tests force splitting on small graphs.
+inline u32 walk_cl() {
+    const char* e = std::getenv("GL_WALK_CL");
+    return e && *e >= '0' && *e <= '9' ? (u32)std::strtoul(e, nullptr, 10) : kWalkCl;
+}
+inline bool piece_forced() {
+    const char* e = std::getenv("GL_PIECE_WEDGES");
+    return e && *e >= '0' && *e <= '9';
+}
+inline u64 piece_cap(u64 wtot, int sms, int world) {
+    if (piece_forced()) return std::max<u64>(1, std::strtoull(std::getenv("GL_PIECE_WEDGES"), nullptr, 10));
+    return std::max<u64>(wtot / (4ull * (u64)sms * (u64)world), 1ull << 17);
 }
 
 struct Timer {
@@ -698,8 +751,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u64 psparse = 0, pbig = 0;
             if (nwin) {
                 u32* np = kin; // scratch: keys are sorted into kout already
-                k_piece_count<<<grid1d(nwin, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), iout, nwin, piece_cap(wtot),
-                                                                    np);
+                k_piece_count<<<grid1d(nwin, 256, sms), 256, 0, s2>>>(
+                    g, cs.wpre.as<u64>(), iout, nwin, piece_cap(wtot, sms, world), piece_forced() ? 1u : 32u, np);
                 GL_CUDA(cudaMemsetAsync(np + nwin, 0, sizeof(u32), s2));
                 u32* poff = cs.items_c.as<u32>() + 2 * (n + 1); // see the allocation above
                 dev_exclusive_scan<u32>(cs.tmp_c, np, poff, nwin + 1, s2);
@@ -710,14 +763,15 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 psparse = hp[0];
                 pbig = hp[1] - hp[0];
                 cs.pieces.alloc(((u64)hp[1] * 2 + 2) * sizeof(uint4)); // all pieces, then this rank's share
-                k_pieces<<<(unsigned)std::min<u64>(nwin, (u64)sms * 8), 256, 0, s2>>>(g, cs.wpre.as<u64>(), iout, nwin,
-                                                                                  poff, cs.pieces.as<uint4>());
+                k_pieces<<<(unsigned)std::min<u64>(nwin, (u64)sms * 8), 256, 0, s2>>>(
+                    g, cs.wpre.as<u64>(), iout, nwin, nsparse, (const unsigned*)(counters + 22), walk_cl(), poff,
+                    cs.pieces.as<uint4>());
                 GL_LAUNCH_CHECK();
                 cs.launches += 4;
                 if (std::getenv("GL_DEBUG"))
                     std::fprintf(stderr, "[gl] cycle pieces: %llu sparse-big, %llu big (from %llu windowed tops, cap %llu)\n",
                                  (unsigned long long)psparse, (unsigned long long)pbig, (unsigned long long)nwin,
-                                 (unsigned long long)piece_cap(wtot));
+                                 (unsigned long long)piece_cap(wtot, sms, world));
             }
             const u64 mysparse_p = rank_share(psparse, rank, world), mybig_p = rank_share(pbig, rank, world);
             uint4* pall = cs.pieces.as<uint4>();
@@ -731,6 +785,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* lsmall = lsmid + mysmid;
             if (mysparse_p || mybig_p || mymid || mysmid) {
                 if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
+                if (g.dmax >= (1u << 24)) throw overflow_error("cycle pass needs max degree < 2^24 (window run counts)");
                 // per-block scratch: big tops need dmax + 2 entries, hash tops at most
                 // their wedge bound (nb <= wedges)
                 const u32 cap_big = (g.dmax + 3) & ~1u;
@@ -738,6 +793,27 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const u64 w_big = (big_scratch_words(cap_big) + 1) & ~1ull;
                 const u64 w_hash = (big_scratch_words(cap_hash) + 1) & ~1ull;
                 if (mybig_p || mysparse_p) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
+                // run-end table of the dense windows (once per graph and walk_cl; GL_RUN_TABLE=0 disables)
+                const char* rt = std::getenv("GL_RUN_TABLE");
+                const bool use_runs = mybig_p && !(rt && rt[0] == '0');
+                if (use_runs && cs.runtab_key != walk_cl() + 1) {
+                    const u64 S = 2 * m;
+                    DevBuf rev;
+                    rev.alloc(S * sizeof(u32));
+                    cs.runtab.alloc(S * sizeof(u32));
+                    k_run_flags<<<grid1d(S, 256, sms, 16), 256, 0, s2>>>(g, tiers, walk_cl(), rev.as<u32>());
+                    k_row_flags<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, rev.as<u32>());
+                    GL_LAUNCH_CHECK();
+                    size_t bytes = 0;
+                    GL_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rev.as<u32>(), cs.runtab.as<u32>(), MinU32{},
+                                                           (int64_t)S, s2));
+                    cs.tmp_c.alloc(bytes);
+                    GL_CUDA(cub::DeviceScan::InclusiveScan(cs.tmp_c.p, bytes, rev.as<u32>(), cs.runtab.as<u32>(),
+                                                           MinU32{}, (int64_t)S, s2));
+                    GL_CUDA(cudaStreamSynchronize(s2)); // rev goes back to the (stream-unaware) pool
+                    cs.runtab_key = walk_cl() + 1;
+                    cs.launches += 3;
+                }
                 if (mymid || mysmid) cs.cursor2.alloc((u64)sms * 4 * w_hash * sizeof(u32));
                 auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
                     constexpr int K = decltype(kind)::value;
@@ -754,7 +830,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
                     smem_attr(k_cycle_block<K>, smem, gr.device);
                     k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s2>>>(
-                        g, list, plist, count, queue, cs.slots.as<i64>(), scratch, cap, tiers);
+                        g, list, plist, count, queue, cs.slots.as<i64>(), scratch, cap, tiers, walk_cl(),
+                        K == 0 && use_runs ? cs.runtab.as<u32>() : nullptr);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };
@@ -936,9 +1013,9 @@ void micro_records(const Graph& gr, u64 first, u64 count, u64* host_out) {
 
 #ifdef GL_CYCLE_PROF
 extern "C" int gl_debug_cycle_profile(unsigned long long* out, int reset) {
-    if (cudaMemcpyFromSymbol(out, gl::g_cycle_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return -4;
+    if (cudaMemcpyFromSymbol(out, gl::g_cycle_prof, sizeof(unsigned long long) * 64) != cudaSuccess) return -4;
     if (reset) {
-        unsigned long long z[32] = {0};
+        unsigned long long z[64] = {0};
         if (cudaMemcpyToSymbol(gl::g_cycle_prof, z, sizeof(z)) != cudaSuccess) return -4;
     }
     return 0;

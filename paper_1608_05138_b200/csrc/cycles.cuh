@@ -185,7 +185,7 @@ __device__ __forceinline__ u64 gallop_lower_bound(const u32* __restrict__ a, u64
 constexpr int kNcBatch = 8; // b's whose window test loads are issued together
 
 #ifdef GL_CYCLE_PROF
-__device__ unsigned long long g_cycle_prof[32]; // [0..10] dense windows, [16..26] mid hash,
+__device__ unsigned long long g_cycle_prof[64]; // [0..10] dense windows, [16..26] mid hash,
                                                 // [12] uniform rounds, [13] mixed rounds (dense)
 #endif
 
@@ -204,6 +204,43 @@ __device__ __forceinline__ u64 gallop_from(const u32* __restrict__ a, u64 lo, u6
         r = p;
         step <<= 1;
     }
+}
+
+// Dense-window grid of a top with nb lower neighbours: windows never cross a
+// degree tier; inside tier [t0, t1) (counter width 32 >> cl bits) they start at
+// t0 + i * span.  span keeps nb * span < 2^31 (window wedge counts and indices
+// are u32).  A fixed grid lets a top's c-range pieces cut on window boundaries
+// (the pieces then hold exactly the windows of the unsplit top).
+// Windows over the low-degree tiers (cl >= kWalkCl: degree < 16, 2- and 4-bit
+// counters) hold short runs (RMAT-24: 2.5 / 5 wedges per run, half of all
+// windows and 42% of the runs for 5.5% of the wedges): there each thread walks
+// its b's runs itself (no run search, no scan, no flattening) and the window
+// spans the whole dynamic shared memory (the run metadata is not needed).
+// walk_cl = the lowest counter tier that walks (default kWalkCl; 5 = never,
+// GL_WALK_CL overrides).
+constexpr u32 kWalkCl = 3;
+constexpr u32 kWalkWords = (kWindow + 3 * 7168) & ~3u; // Cyc<0>: WORDS + 3 * META (+1 unused)
+__host__ __device__ __forceinline__ u64 win_span(u32 cl, u64 nb, u32 walk_cl) {
+    if (cl >= walk_cl) return (u64)kWalkWords << cl;
+    u64 span = (u64)kWindow << cl;
+    // window wedges are scanned in 40 bits (nb * span bounds them); a window
+    // that comes out above 2^31 wedges (u32 walk indices) is re-cut at run time
+    if (nb * span >= (1ull << 40)) span = ((1ull << 40) / nb) & ~31ull;
+    return span;
+}
+__device__ __forceinline__ u32 tier_of(u32 c, uint4 tiers, u32& t0, u32& t1) {
+    if (c < tiers.x) { t0 = 0; t1 = tiers.x; return 4; }
+    if (c < tiers.y) { t0 = tiers.x; t1 = tiers.y; return 3; }
+    if (c < tiers.z) { t0 = tiers.y; t1 = tiers.z; return 2; }
+    if (c < tiers.w) { t0 = tiers.z; t1 = tiers.w; return 1; }
+    t0 = tiers.w;
+    t1 = 0xffffffffu;
+    return 0;
+}
+__device__ __forceinline__ u32 grid_floor(u32 c, uint4 tiers, u64 nb, u32 walk_cl) {
+    u32 t0, t1;
+    const u64 span = win_span(tier_of(c, tiers, t0, t1), nb, walk_cl);
+    return t0 + (u32)(((u64)(c - t0) / span) * span);
 }
 
 // per-block scratch layout (cap = dmax + 2 entries each, cap even)
@@ -542,11 +579,111 @@ __device__ __forceinline__ void meta_pass(const DevGraph& g, const RunMeta& Msm,
     }
 }
 
+// Thread-walk window [lo, hi) of a dense top (low-degree tiers): each thread
+// walks the runs of its b's (b = thread + i * THREADS) from the cursor while
+// c < hi -- pass 0 increments W and finds the run end as it goes, pass 1
+// re-walks the run crediting W-1 to (b,c) and the run's sum to (a,b); then the
+// used window words are bulk-cleared.  Four entries of a row are loaded per
+// step (one sector, independent loads).
+constexpr int kWalkStep = 4;
+__device__ __noinline__ void walk_window(const DevGraph& g, const BigScratch& S, u32 nb, u32* W, u32 lo, u32 hi,
+                                            u32 cl, u32 win, u64 abase, i64* __restrict__ slot_acc) {
+    const u32 wb = smem_u32(W);
+    const u32 T = blockDim.x;
+#ifdef GL_CYCLE_PROF
+    u32 pr = 0, pw = 0;
+#endif
+    // pass 0: kNcBatch cursor-c loads in flight, then walk the active b's
+    for (u32 j0 = threadIdx.x; j0 < nb; j0 += kNcBatch * T) {
+        u32 nc[kNcBatch];
+#pragma unroll
+        for (int u = 0; u < kNcBatch; ++u) nc[u] = j0 + u * T < nb ? S.nextc[j0 + u * T] : kEmpty;
+#pragma unroll 1
+        for (int u = 0; u < kNcBatch; ++u) {
+            u32 c = nc[u];
+            if (c >= hi) continue; // kEmpty >= hi
+            const u32 j = j0 + u * T;
+            const u64 rb = S.rb[j];
+            const u32 re = S.rend[j], h0 = S.cur[j];
+            u32 h = h0;
+            for (;;) {
+                u32 nx[kWalkStep];
+#pragma unroll
+                for (int v = 0; v < kWalkStep; ++v) nx[v] = h + 1 + v < re ? __ldg(g.adj + rb + h + 1 + v) : kEmpty;
+                bool stop = false;
+#pragma unroll
+                for (int v = 0; v < kWalkStep; ++v) {
+                    if (!stop) {
+                        const u32 ci = c - lo;
+                        red_shared_add(wb + ((ci >> cl) << 2), 1u << ((ci & ((1u << cl) - 1u)) << (5 - cl)));
+                        ++h;
+                        c = nx[v];
+                        stop = c >= hi;
+                    }
+                }
+                if (stop) break;
+            }
+#ifdef GL_CYCLE_PROF
+            ++pr;
+            pw += h - h0;
+#endif
+            S.hpos[j] = h0;
+            S.cur[j] = h;
+            S.nextc[j] = c; // >= hi or kEmpty
+            S.rwin[j] = win;
+        }
+    }
+#ifdef GL_CYCLE_PROF
+    pr = __reduce_add_sync(0xffffffffu, pr);
+    pw = __reduce_add_sync(0xffffffffu, pw);
+    if (lane_id() == 0) {
+        atomicAdd(&g_cycle_prof[33 + 4 * cl], (unsigned long long)pr);
+        atomicAdd(&g_cycle_prof[34 + 4 * cl], (unsigned long long)pw);
+    }
+    if (threadIdx.x == 0) atomicAdd(&g_cycle_prof[32 + 4 * cl], 1ull);
+#endif
+    __syncthreads();
+    // pass 1: re-walk the runs of this window, W-1 to (b,c), the run's sum to (a,b)
+    for (u32 j0 = threadIdx.x; j0 < nb; j0 += kNcBatch * T) {
+        u32 rw[kNcBatch];
+#pragma unroll
+        for (int u = 0; u < kNcBatch; ++u) rw[u] = j0 + u * T < nb ? S.rwin[j0 + u * T] : kEmpty;
+#pragma unroll 1
+        for (int u = 0; u < kNcBatch; ++u) {
+            if (rw[u] != win) continue;
+            const u32 j = j0 + u * T;
+            const u64 rb = S.rb[j];
+            const u32 h1 = S.cur[j];
+            u64 sum = 0;
+            for (u32 p = S.hpos[j]; p < h1; p += kWalkStep) {
+                u32 cv[kWalkStep];
+#pragma unroll
+                for (int v = 0; v < kWalkStep; ++v) cv[v] = p + v < h1 ? __ldg(g.adj + rb + p + v) : kEmpty;
+#pragma unroll
+                for (int v = 0; v < kWalkStep; ++v) {
+                    if (cv[v] != kEmpty) {
+                        const u32 ci = cv[v] - lo;
+                        const u32 w = ld_shared(wb + ((ci >> cl) << 2)) >> ((ci & ((1u << cl) - 1u)) << (5 - cl));
+                        const u32 val = (w & ((1u << (32u >> cl)) - 1u)) - 1u;
+                        red_add_u64_if(&slot_acc[rb + p + v], (u64)val);
+                        sum += val;
+                    }
+                }
+            }
+            if (sum) atomic_add_i64(&slot_acc[abase + j], (i64)sum);
+        }
+    }
+    __syncthreads();
+    const u32 words = (hi - lo + (1u << cl) - 1u) >> cl;
+    table_clear(W, (words + 3u) & ~3u, 0u, T);
+    __syncthreads();
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict__ pieces, u64 n_items,
               unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap,
-              uint4 tiers) {
+              uint4 tiers, u32 walk_cl, const u32* __restrict__ nxt_rev) {
     constexpr bool HASH = Cyc<KIND>::HASH, WIN = Cyc<KIND>::WIN;
     constexpr int THREADS = Cyc<KIND>::THREADS;
     constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
@@ -591,7 +728,10 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
         // c-range pieces that different blocks (and ranks) take; every credit is
         // an atomic add, so the pieces of a top sum exactly
         uint4 pc = make_uint4(0, 0, 0, 0);
-        if constexpr (WIN) pc = pieces[idx];
+        if constexpr (WIN) {
+            pc = pieces[idx];
+            if (pc.x == kEmpty) continue; // empty piece (its cut points coincided)
+        }
         const u32 a = WIN ? pc.x : items[idx];
         const u32 clo = pc.y, chi = WIN ? pc.z : a;
         const u64 E0 = g.loff[a];
@@ -658,10 +798,20 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
             S.rb[j] = rb;
             S.rend[j] = re;
             u32 c0 = 0;
-            if (clo && re) c0 = g.adj[rb + re - 1] < clo ? re : (u32)(lower_bound_dev<u32, u64>(g.adj, rb, rb + re, clo) - rb);
+            const u32 lc = re > 0 ? g.adj[rb + re - 1] : 0u;
+            if (clo && re) {
+                // seek the piece's first c: gallop from an interpolated position
+                const u32 fc = g.adj[rb];
+                if (lc < clo) {
+                    c0 = re;
+                } else if (fc < clo) {
+                    const u64 hint = (u64)(re - 1) * (clo - fc) / (lc - fc);
+                    c0 = (u32)(gallop_from(g.adj, rb, rb + re, rb + hint, clo) - rb);
+                }
+            }
             S.cur[j] = c0;
             const u32 c = c0 < re ? g.adj[rb + c0] : kEmpty;
-            if (WIN) S.lastc[j] = re > 0 ? g.adj[rb + re - 1] : 0u;
+            if (WIN) S.lastc[j] = lc;
             S.nextc[j] = c < chi ? c : kEmpty;
             S.rwin[j] = kEmpty;
             S.plen[j] = 0;
@@ -675,7 +825,15 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
         // value under it (nextc), so a window only gallops the b's whose next c
         // falls inside it; for the others one coalesced nextc load suffices.
         u32 win = 0;
-        for (u32 lo = s_next, hi = 0; lo < chi; lo = hi, ++win) {
+        bool meta_dirty = true; // block-uniform: run metadata may sit in the walk windows' words
+        // dense windows start on the top's window grid (so pieces cut on grid
+        // points reproduce the unsplit top's windows); hash windows at s_next
+        u32 lo0 = s_next;
+        if (!HASH && lo0 < chi) {
+            lo0 = grid_floor(lo0, tiers, nb, walk_cl);
+            lo0 = lo0 > clo ? lo0 : clo;
+        }
+        for (u32 lo = lo0, hi = 0; lo < chi; lo = hi, ++win) {
             // window [lo, hi): inside one degree tier, counters of that tier's width
             u32 cl = 1, tend = chi;
             if (!HASH) {
@@ -683,17 +841,37 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                 tend = lo < tiers.x ? tiers.x : lo < tiers.y ? tiers.y : lo < tiers.z ? tiers.z : lo < tiers.w ? tiers.w : chi;
                 tend = tend < chi ? tend : chi;
             }
-            u64 span = (u64)kWindow << cl;
+            u64 span = win_span(cl, nb, walk_cl);
             if (KIND == 3) { // about kHashWinTarget wedges if they were uniform over [lo, chi)
                 span = rem ? (u64)(chi - lo) * kHashWinTarget / rem : (u64)(chi - lo);
                 span = span ? span : 1;
+                // keep nb * span < 2^31: window wedge counts and indices are u32
+                if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
             }
-            // keep nb * span < 2^31: window wedge counts and indices are u32
-            if ((u64)nb * span >= (1ull << 31)) span = ((1ull << 31) / nb) & ~31ull;
             hi = !WIN ? a : (u32)std::min<u64>(std::min<u64>((u64)lo + span, (u64)tend), (u64)chi);
 
-            u32 my_runs, my_wedges, nnz, T;
-            u64 mine;
+            if constexpr (!HASH) {
+                if (cl >= walk_cl) {
+                    // short runs: thread-walk window (see kWalkCl).  The window
+                    // words reach into the run-metadata area: clear it first if a
+                    // flattened window of the previous top used it.
+                    if (meta_dirty) {
+                        table_clear(W + kWords, kWalkWords - kWords, 0u, THREADS);
+                        __syncthreads();
+                        meta_dirty = false;
+                    }
+                    walk_window(g, S, nb, W, lo, hi, cl, win, abase, slot_acc);
+                    GL_PROF_MARK(3);
+                    continue;
+                }
+            }
+            u32 my_runs, nnz, T;
+            u64 my_wedges, mine;
+            constexpr u32 kRunShift = 40; // (runs << 40) | wedges: runs <= nb < 2^24 (host check)
+            // run ends from the per-slot next-window table (k_run_table): one
+            // load instead of a gallop, when this window is on the global grid
+            // (not re-cut, top below the span clamp)
+            bool grid_ends = KIND == 0 && nxt_rev != nullptr && (u64)nb * ((u64)kWalkWords << 4) < (1ull << 40);
             for (;;) {
                 // run ends of the b's with a c in [lo, hi); runs are ordered
                 // thread-major (thread t owns b = t + i*THREADS), so one block scan
@@ -715,9 +893,17 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                         u32 h = re;
                         // the row's last window needs no search: its run ends at re
                         if (WIN && S.lastc[j] >= hi) {
-                            const u32 pl = S.plen[j];
-                            h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
-                            S.plen[j] = h - c0;
+                            if (grid_ends) {
+                                // first slot after rb + c0 on a later window (or row start)
+                                const u64 p1 = rb + c0 + 1;
+                                const u32 q = p1 < 2 * g.m ? nxt_rev[2 * g.m - 1 - p1] : kEmpty;
+                                const u64 qe = (u64)q - rb;
+                                h = qe < (u64)re ? (u32)qe : re;
+                            } else {
+                                const u32 pl = S.plen[j];
+                                h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
+                                S.plen[j] = h - c0;
+                            }
                         }
                         S.hpos[j] = c0; // run start
                         S.rwin[j] = win;
@@ -729,13 +915,33 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                 }
                 GL_PROF_SYNC_MARK(6);
                 u64 tot;
-                mine = ((u64)my_runs << 32) | my_wedges;
+                mine = ((u64)my_runs << kRunShift) | my_wedges;
                 {
                     using BlockScan = cub::BlockScan<u64, THREADS>;
                     __shared__ typename BlockScan::TempStorage tmp;
                     BlockScan(tmp).ExclusiveSum(mine, mine, tot);
                 }
-                nnz = (u32)(tot >> 32), T = (u32)tot;
+                nnz = (u32)(tot >> kRunShift);
+                const u64 T64 = tot & ((1ull << kRunShift) - 1);
+                T = (u32)T64;
+                // a dense window above 2^31 wedges (u32 walk indices; only a
+                // top with a huge lower neighbourhood): restore its b's cursors
+                // and halve it (the run ends are then off the window grid: the
+                // gallop finds them)
+                if constexpr (KIND == 0) {
+                    if (T64 < (1ull << 31)) break;
+                    for (u32 j = threadIdx.x; j < nb; j += THREADS) {
+                        if (S.rwin[j] != win) continue;
+                        const u32 c0 = S.hpos[j];
+                        S.cur[j] = c0;
+                        S.nextc[j] = g.adj[S.rb[j] + c0];
+                        S.rwin[j] = kEmpty;
+                    }
+                    __syncthreads(); // BlockScan storage reuse
+                    hi = lo + std::max<u32>((hi - lo) / 2, 32u);
+                    grid_ends = false;
+                    continue;
+                }
                 // a KIND 3 window over its wedge cap: restore its b's cursors
                 // and re-cut it narrower (a window of <= kHashWinMax ids is
                 // always accepted: its distinct c ids fit the slots anyway)
@@ -770,6 +976,10 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
             GL_PROF_ADD(9, T);
 #ifdef GL_CYCLE_PROF
             if (KIND == 0 && threadIdx.x == 0) {
+                // per counter tier cl (4 = 2-bit ... 0 = 32-bit): windows, runs, wedges
+                atomicAdd(&g_cycle_prof[32 + 4 * cl], 1ull);
+                atomicAdd(&g_cycle_prof[33 + 4 * cl], (unsigned long long)nnz);
+                atomicAdd(&g_cycle_prof[34 + 4 * cl], (unsigned long long)T);
                 atomicAdd(&g_cycle_prof[11], (unsigned long long)nnz);
                 if (nnz > kMeta) {
                     atomicAdd(&g_cycle_prof[14], 1ull);
@@ -778,9 +988,10 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
             }
 #endif
             const RunMeta M = nnz <= kMeta ? Msm : Mgl;
+            if (!HASH) meta_dirty = true;
             if (my_runs) {
-                u32 q = (u32)(mine >> 32), w = (u32)mine;
-                for (u32 j0 = threadIdx.x; j0 < nb && q < (u32)(mine >> 32) + my_runs; j0 += kNcBatch * THREADS) {
+                u32 q = (u32)(mine >> kRunShift), w = (u32)(mine & ((1ull << kRunShift) - 1));
+                for (u32 j0 = threadIdx.x; j0 < nb && q < (u32)(mine >> kRunShift) + my_runs; j0 += kNcBatch * THREADS) {
                     u32 rw[kNcBatch];
 #pragma unroll
                     for (int u = 0; u < kNcBatch; ++u) {

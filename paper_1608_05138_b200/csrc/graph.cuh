@@ -84,6 +84,8 @@ struct CountState {
     DevBuf keys_c, items_c, tmp_c; // the cycle pass's own (it runs concurrently on s2)
     DevBuf pieces;                 // uint4 (a, clo, chi, wedge estimate): windowed-top pieces, then the rank's share
     u64 cycle_pieces = 0;
+    DevBuf runtab;                 // u32[2m] run-end table of the dense cycle windows (count.cu k_run_flags)
+    u32 runtab_key = 0;            // walk_cl + 1 it was built for (0: none)
     cudaStream_t s2 = nullptr;     // cycle-pass stream (owned)
     cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork, 7 end of count_mid
     u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0, n_items3x = 0;

@@ -15,7 +15,7 @@ from test_gpu_parity import recut_graph  # noqa: E402
 cases = [("ba", 60000, 6, 3), ("ba", 200000, 4, 11), ("ba", 30000, 12, 5), ("recut", 0, 0, 1)]
 for kind, n, k, seed in cases:
     g = gl.Graph.build(recut_graph(seed) if kind == "recut" else gl.generate_ba(n, k, seed=seed))
-    buf = (C.c_ulonglong * 32)()
+    buf = (C.c_ulonglong * 64)()
     prof = hasattr(gl.LIB, "gl_debug_cycle_profile") and "prof" in os.environ.get("GRAPHLET_B200_LIB", "")
     if prof:
         gl.LIB.gl_debug_cycle_profile(buf, 1)

@@ -21,7 +21,7 @@ def run():
 
 
 run()
-buf = (C.c_ulonglong * 32)()
+buf = (C.c_ulonglong * 64)()
 gl.LIB.gl_debug_cycle_profile(buf, 1)
 run()
 gl.LIB.gl_debug_cycle_profile(buf, 0)
@@ -39,3 +39,11 @@ for base, kind in ((0, "dense windows"), (16, "mid hash")):
     w, T, tops = buf[base + 8], buf[base + 9], buf[base + 10]
     print(f"  windows {w}  wedges {T}  tops {tops}  wedges/window {T / max(1, w):.0f}")
 print(f"windowed-hash (sparse big) windows {buf[30]}  wedges {buf[31]}  re-cuts {buf[29]}")
+print("dense windows per counter tier (bits: windows, runs, wedges, wedges/run):")
+for cl in range(5):
+    w, r, T = buf[32 + 4 * cl], buf[33 + 4 * cl], buf[34 + 4 * cl]
+    print(f"  {32 >> cl:2d}-bit  {w:10d} {r:14d} {T:16d} {T / max(1, r):8.1f}")
+ms, _, _ = g.last_stats()
+print("phase ms (last count):", ms)
+pc = g.cycle_pieces()
+print(f"cycle pieces {len(pc)} from {len(set(pc[:, 0].tolist()))} windowed tops; max estimate {pc[:, 3].max() if len(pc) else 0}")

@@ -169,9 +169,10 @@ int gl_edge_counts(const gl_graph *g, uint64_t first, uint64_t count, uint32_t *
 int gl_edge_counts_device(const gl_graph *g, const uint32_t **t, const uint64_t **x7,
                           const uint64_t **x10);
 
-/* The cycle pass runs on its own stream concurrently with the clique /
- * triangle pass (default 1); 0 serialises them on the caller's stream, e.g.
- * to time each pass alone. Process-wide. */
+/* 1: the cycle pass runs on its own stream concurrently with the clique /
+ * triangle pass; 0 (default; concurrency measured slower on B200: both
+ * passes fill every SM and share L2) runs them one after the other on the
+ * caller's stream. Process-wide. */
 int gl_set_overlap(int on);
 
 /* Kernel timing of the last count call (CUDA events on the launching stream),

@@ -301,6 +301,12 @@ Graph* build_graph_device(const u64* d_pairs, u64 count, int device) {
         }
         // eid_t is u32 in the reference (common.hpp:14): m < 2^32 - 1
         if (m >= id_limit("GL_TEST_EDGE_LIMIT")) throw invalid_argument("graph exceeds 32-bit edge id space");
+        // device counting carries adjacency slots (2m of them) in 32 bits: the
+        // reference's u32 edge ids admit m < 2^32 - 1, this path m < 2^31.
+        // Refused here, at load time, with the reference's invalid_argument
+        // (GL_TEST_SLOT_LIMIT lowers the 2^32 slot bound for the tests)
+        if (2 * m >= id_limit("GL_TEST_SLOT_LIMIT") + 1)
+            throw invalid_argument("graph exceeds the device counting limit (2m adjacency slots < 2^32)");
         keys_b.reset();
         ltab.reset();
         const u64* ekeys = keys_a.as<u64>();

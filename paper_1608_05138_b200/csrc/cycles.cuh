@@ -144,6 +144,9 @@ __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_gene
 __device__ __forceinline__ void red_shared_add(u32 addr, u32 v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_shared(u32 addr, u32 v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ u32 ld_shared(u32 addr) {
     u32 v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -344,11 +347,11 @@ __device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, u32 cl) {
 __device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, u32 cl) { W[(c - lo) >> cl] = 0; }
 
 template <int KIND, int PASS>
-__device__ __forceinline__ void wedge_op(u32* W, u32 cv, u32 lo, u32 cl, i64* __restrict__ slot_acc, u64 slot,
+__device__ __forceinline__ void wedge_op(u32* W, u32 wb, u32 cv, u32 lo, u32 cl, i64* __restrict__ slot_acc, u64 slot,
                                          u64& val) {
-    if (!Cyc<KIND>::HASH) { // dense window: 32-bit shared addresses, predicated RED
+    if (!Cyc<KIND>::HASH) { // dense window: 32-bit shared addresses (wb = W's), predicated RED
         const u32 ci = cv - lo;
-        const u32 addr = smem_u32(W) + ((ci >> cl) << 2);
+        const u32 addr = wb + ((ci >> cl) << 2);
         const u32 sh = (ci & ((1u << cl) - 1u)) << (5 - cl);
         if (PASS == 0) {
             red_shared_add(addr, 1u << sh);
@@ -408,6 +411,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                                             u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
     const u32 lane = lane_id();
     if (kb >= ke) return;
+    const u32 wb = smem_u32(W);
     u32 bs = warp_upper_bound(S.pre, nnz + 1, kb);
     u32 k0 = kb;
     while (k0 < ke) {
@@ -422,28 +426,51 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
 #endif
             const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
             u64 acc = 0;
-            // software pipeline: the next kHalf rounds' loads are in flight
-            // while the current kHalf rounds update the window
+            // every round of the stretch is full: branch-free wedge ops on a
+            // hoisted shared base (dense windows), groups of kHalf rounds with
+            // the next group's loads in flight, then up to kHalf-1 tail rounds
             constexpr int kHalf = kUnroll / 2;
-            u32 cv[kHalf];
-#pragma unroll
-            for (int u = 0; u < kHalf; ++u) cv[u] = (u32)u < nfull ? __ldg(g.adj + sbase + 32u * u) : kEmpty;
-            for (u32 r = 0; r < nfull; r += kHalf) {
-                u32 nx[kHalf];
-#pragma unroll
-                for (int u = 0; u < kHalf; ++u)
-                    nx[u] = r + kHalf + u < nfull ? __ldg(g.adj + sbase + 32u * (r + kHalf + u)) : kEmpty;
-#pragma unroll
-                for (int u = 0; u < kHalf; ++u) {
-                    if (cv[u] != kEmpty) {
-                        u64 v = 0;
-                        wedge_op<KIND, PASS>(W, cv[u], lo, cl, slot_acc, sbase + 32u * (r + u), v);
+            const u32* __restrict__ src = g.adj + sbase;
+            auto op = [&](u32 cv, u32 r) {
+                if constexpr (!Cyc<KIND>::HASH) {
+                    const u32 ci = cv - lo;
+                    const u32 addr = wb + ((ci >> cl) << 2);
+                    const u32 sh = (ci & ((1u << cl) - 1u)) << (5 - cl);
+                    if (PASS == 0) {
+                        red_shared_add(addr, 1u << sh);
+                    } else if (PASS == 1) {
+                        const u32 w = ld_shared(addr) >> sh;
+                        const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
+                        red_add_u64_if(&slot_acc[sbase + 32u * r], (u64)v);
                         acc += v;
+                    } else {
+                        st_shared(addr, 0u);
                     }
+                } else {
+                    u64 v = 0;
+                    wedge_op<KIND, PASS>(W, wb, cv, lo, cl, slot_acc, sbase + 32u * r, v);
+                    acc += v;
+                }
+            };
+            u32 r = 0;
+            if (nfull >= (u32)kHalf) {
+                u32 cv[kHalf];
+#pragma unroll
+                for (int u = 0; u < kHalf; ++u) cv[u] = __ldg(src + 32u * u);
+                for (; r + 2 * kHalf <= nfull; r += kHalf) {
+                    u32 nx[kHalf];
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u) nx[u] = __ldg(src + 32u * (r + kHalf + u));
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u) cv[u] = nx[u];
                 }
 #pragma unroll
-                for (int u = 0; u < kHalf; ++u) cv[u] = nx[u];
+                for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
+                r += kHalf;
             }
+            for (; r < nfull; ++r) op(__ldg(src + 32u * r), r);
             if (PASS == 1) {
                 acc = warp_sum_u64(acc);
                 if (lane == 0 && acc) atomic_add_i64(&slot_acc[abase + S.rj[bs]], (i64)acc);
@@ -471,7 +498,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             u64 v = 0;
             if (valid) {
                 const u64 slot = (u64)S.rs[q] + off;
-                wedge_op<KIND, PASS>(W, __ldg(g.adj + slot), lo, cl, slot_acc, slot, v);
+                wedge_op<KIND, PASS>(W, wb, __ldg(g.adj + slot), lo, cl, slot_acc, slot, v);
             }
             if (PASS == 1) {
                 const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));

@@ -25,6 +25,27 @@ def test_edge_id_space_is_invalid_argument(cuda_device, monkeypatch):
         gl.Graph.build(np.array([[0, 1], [1, 2], [2, 0]], np.uint64), cuda_device)
 
 
+def test_slot_limit_is_invalid_argument(cuda_device, monkeypatch):
+    """Device counting needs 2m < 2^32 adjacency slots: refused at load time
+    with the reference's invalid_argument (GL_TEST_SLOT_LIMIT lowers 2^32-1)."""
+    monkeypatch.setenv("GL_TEST_SLOT_LIMIT", "5")
+    gl.Graph.build(np.array([[0, 1], [1, 2]], np.uint64), cuda_device)  # 2m = 4 < 6
+    with pytest.raises(gl.InvalidArgument, match="counting limit"):
+        gl.Graph.build(np.array([[0, 1], [1, 2], [2, 0]], np.uint64), cuda_device)  # 2m = 6
+
+
+def test_degree_limit_is_overflow(cuda_device, monkeypatch):
+    """The cycle windows count runs in 24 bits: max degree >= 2^24 is refused
+    (GL_ERR_OVERFLOW) rather than miscounted (GL_TEST_DEGREE_LIMIT lowers it)."""
+    star = np.array([[0, i] for i in range(1, 200)] + [[1, 2], [3, 4], [2, 3]], np.uint64)
+    g = gl.Graph.build(star, cuda_device)
+    monkeypatch.setenv("GL_TEST_DEGREE_LIMIT", "150")
+    with pytest.raises(gl.CountOverflowError, match="max degree"):
+        g.count()
+    monkeypatch.delenv("GL_TEST_DEGREE_LIMIT")
+    assert g.count().X[1] == g.num_edges()
+
+
 def test_call_sequence_errors(cuda_device):
     import torch
     g = gl.Graph.build(gl.generate_rmat(10, 8, seed=2), cuda_device)

@@ -159,6 +159,17 @@ int gl_global_from_unrestricted(const gl_unrestricted *c, uint64_t n, uint64_t m
 /* micro_counts (counts.hpp:90; counts.cpp:122-136) for edge ids
  * [first, first+count) of the last gl_count / gl_count_finish shard. */
 int gl_micro_records(const gl_graph *g, uint64_t first, uint64_t count, gl_micro_record *out);
+/* EdgeMotifRecord (counts.hpp:20-35) of process_edge_hash (kernels.cpp:143-156)
+ * for edge ids [first, first+count) of the last count's shard: t, s_u, s_v,
+ * x7, x10 and the reference's deterministic operation counter, which for the
+ * hash pipeline is closed-form: work_units = deg(u) + deg(v) + sum of deg(w)
+ * over w in N(u) (three_graphlets_hash reads N(v) and N(u), derive_s_v
+ * N(v), clique_hash / cycle_hash N(w) for w in T u S_u = N(u) \ {v}). */
+typedef struct {
+    uint32_t edge_id, t, s_u, s_v;
+    uint64_t x7, x10, work_units;
+} gl_edge_motif_record;
+int gl_edge_motif_records(const gl_graph *g, uint64_t first, uint64_t count, gl_edge_motif_record *out);
 /* Compact per-edge output (SoA, host): t, x7, x10 for edge ids
  * [first, first+count); any pointer may be NULL.  The other MicroRecord
  * fields are closed-form in (t, deg(u), deg(v), n) -- counts.cpp:113-136. */

@@ -13,14 +13,26 @@
 //   per-edge loop + accumulate/merge +      count(g) -> Counts{global, unrestricted}
 //     global_from_unrestricted
 //   MicroRecord + micro_counts              MicroRecord, micro_records(g)  (counts.hpp:82-90)
+//   EdgeMotifRecord + process_edge_hash     EdgeMotifRecord, edge_motif_records(g), process_edge_hash(g, e)
+//                                           (counts.hpp:20-35, kernels.hpp:99-102; work_units = the
+//                                           hash pipeline's operation counter, closed form)
+//   LocalThree + local_three_counts         same                           (counts.hpp:73-78)
+//   Graph::degree / neighbors (degree-      same, on a host copy of the CSR loaded on first use
+//     descending view) / neighbors_by_id /  (graph.hpp:56-79)
+//     has_edge / original_label /
+//     internal_id / degree_order_less
 //   graphlet_name(i)                        graphlet_name(i)               (counts.hpp:64)
 //   count_consistency_error,                same; CUDA failures -> cuda_error
 //     count_overflow_error
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <istream>
+#include <memory>
+#include <span>
+#include <unordered_map>
 #include <iterator>
 #include <stdexcept>
 #include <string>
@@ -141,6 +153,26 @@ struct OrientedEdge {
     vid_t u = 0; // low-degree endpoint
     eid_t id = 0;
 };
+struct EdgeMotifRecord {
+    eid_t edge_id = 0;
+    std::uint32_t t = 0;
+    std::uint32_t s_u = 0;
+    std::uint32_t s_v = 0;
+    std::uint64_t x7 = 0;
+    std::uint64_t x10 = 0;
+    std::uint64_t work_units = 0;
+
+    std::uint32_t x3() const { return t; }
+    std::uint64_t disconnected(std::uint64_t n) const { return n - ((std::uint64_t)s_u + s_v + t) - 2; }
+};
+struct LocalThree {
+    std::uint64_t x3 = 0, x4 = 0, x5 = 0;
+};
+// counts.cpp:113-120
+inline LocalThree local_three_counts(const EdgeMotifRecord& rec, std::uint64_t n) {
+    if (n < 2) throw std::invalid_argument("local counts need at least two vertices");
+    return LocalThree{rec.t, (std::uint64_t)rec.s_u + rec.s_v, rec.disconnected(n)};
+}
 
 namespace detail {
 inline count_t u128(const gl_u128& v) { return ((count_t)v.hi << 64) | v.lo; }
@@ -196,9 +228,10 @@ class Graph {
 public:
     Graph() = default;
     explicit Graph(gl_graph* h) : h_(h) {}
-    Graph(Graph&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    Graph(Graph&& o) noexcept : h_(o.h_), host_(std::move(o.host_)) { o.h_ = nullptr; }
     Graph& operator=(Graph&& o) noexcept {
         std::swap(h_, o.h_);
+        std::swap(host_, o.host_);
         return *this;
     }
     Graph(const Graph&) = delete;
@@ -222,8 +255,60 @@ public:
     }
     gl_graph* handle() const { return h_; }
 
+    // graph.hpp:56-79 accessors, served from a host copy of the CSR (loaded on
+    // first use; the device graph is immutable)
+    std::uint32_t degree(vid_t v) const { return host().deg.at(v); }
+    std::span<const vid_t> neighbors_by_id(vid_t v) const {
+        const Host& h = host();
+        return {h.adj.data() + h.off.at(v), h.adj.data() + h.off.at(v + 1)};
+    }
+    // degree descending, ties by ascending id (the reference's P2 view)
+    std::span<const vid_t> neighbors(vid_t v) const {
+        const Host& h = host();
+        return {h.adj_deg.data() + h.off.at(v), h.adj_deg.data() + h.off.at(v + 1)};
+    }
+    bool has_edge(vid_t a, vid_t b) const {
+        const auto r = neighbors_by_id(a);
+        return std::binary_search(r.begin(), r.end(), b);
+    }
+    std::uint64_t original_label(vid_t v) const { return host().label.at(v); }
+    // throws std::out_of_range for an unknown label, like relabel_map_.at
+    vid_t internal_id(std::uint64_t label) const { return host().relabel.at(label); }
+    bool degree_order_less(vid_t a, vid_t b) const {
+        const Host& h = host();
+        return h.deg[a] != h.deg[b] ? h.deg[a] > h.deg[b] : a < b;
+    }
+
 private:
+    struct Host {
+        std::vector<std::uint64_t> off, label;
+        std::vector<vid_t> adj, adj_deg;
+        std::vector<std::uint32_t> deg;
+        std::unordered_map<std::uint64_t, vid_t> relabel;
+    };
+    const Host& host() const {
+        if (!host_) {
+            auto h = std::make_shared<Host>();
+            const std::uint64_t n = num_vertices();
+            h->off.resize(n + 1);
+            h->deg.resize(n);
+            h->label.resize(n);
+            check(gl_graph_degrees(h_, h->deg.data()));
+            check(gl_graph_labels(h_, h->label.data()));
+            h->adj.resize(2 * num_edges());
+            check(gl_graph_csr(h_, h->off.data(), h->adj.data()));
+            h->adj_deg = h->adj;
+            for (std::uint64_t v = 0; v < n; ++v)
+                std::sort(h->adj_deg.begin() + h->off[v], h->adj_deg.begin() + h->off[v + 1],
+                          [&](vid_t a, vid_t b) { return h->deg[a] != h->deg[b] ? h->deg[a] > h->deg[b] : a < b; });
+            h->relabel.reserve(n);
+            for (std::uint64_t v = 0; v < n; ++v) h->relabel.emplace(h->label[v], (vid_t)v);
+            host_ = std::move(h);
+        }
+        return *host_;
+    }
     gl_graph* h_ = nullptr;
+    mutable std::shared_ptr<Host> host_;
 };
 
 // graph.cpp:93-172, executed on `device`
@@ -274,6 +359,26 @@ inline std::vector<MicroRecord> micro_records(const Graph& g, std::uint64_t firs
         out[i] = MicroRecord{r.edge_id, r.x3, r.x4, r.x5, r.x7, r.x10, r.t, r.s_u, r.s_v, r.d_e};
     }
     return out;
+}
+
+// EdgeMotifRecord of every edge id in [first, first+n) (after count(g)):
+// process_edge_hash's record, kernels.cpp:143-156, work_units included
+inline std::vector<EdgeMotifRecord> edge_motif_records(const Graph& g, std::uint64_t first = 0,
+                                                       std::uint64_t n = ~0ull) {
+    const std::uint64_t m = g.num_edges();
+    if (n == ~0ull) n = first < m ? m - first : 0;
+    std::vector<gl_edge_motif_record> raw(n);
+    if (n) check(gl_edge_motif_records(g.handle(), first, n, raw.data()));
+    std::vector<EdgeMotifRecord> out(n);
+    for (std::uint64_t i = 0; i < n; ++i) {
+        const gl_edge_motif_record& r = raw[i];
+        out[i] = EdgeMotifRecord{r.edge_id, r.t, r.s_u, r.s_v, r.x7, r.x10, r.work_units};
+    }
+    return out;
+}
+// kernels.cpp:143-156 for one oriented edge (after count(g))
+inline EdgeMotifRecord process_edge_hash(const Graph& g, const OrientedEdge& e) {
+    return edge_motif_records(g, e.id, 1).at(0);
 }
 
 } // namespace b200

@@ -31,7 +31,7 @@ __all__ = [
     "GraphletError", "ParseError", "CountConsistencyError", "CountOverflowError",
     "CudaError", "Graph", "load_edge_list", "load_edge_list_file", "generate_rmat",
     "generate_rmat_device", "generate_gnm", "generate_ba", "global_from_unrestricted",
-    "graphlet_name", "GRAPHLET_NAMES", "MICRO_DTYPE", "lib_path", "LIB",
+    "graphlet_name", "GRAPHLET_NAMES", "MICRO_DTYPE", "MOTIF_DTYPE", "local_three_counts", "lib_path", "LIB",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -68,6 +68,9 @@ class _UC(C.Structure):
 
 MICRO_FIELDS = ("edge_id", "x3", "x4", "x5", "x7", "x10", "t", "s_u", "s_v", "d_e")
 MICRO_DTYPE = np.dtype([(f, "<u8") for f in MICRO_FIELDS])
+# EdgeMotifRecord (counts.hpp:20-35), hash pipeline (kernels.cpp:143-156)
+MOTIF_DTYPE = np.dtype([("edge_id", "<u4"), ("t", "<u4"), ("s_u", "<u4"), ("s_v", "<u4"),
+                        ("x7", "<u8"), ("x10", "<u8"), ("work_units", "<u8")])
 
 GRAPHLET_NAMES = {
     1: "edge", 2: "2-node-independent", 3: "triangle", 4: "2-star", 5: "3-node-1-edge",
@@ -120,6 +123,7 @@ _sig("gl_count_finish", C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
      C.POINTER(_UC), C.c_void_p)
 _sig("gl_global_from_unrestricted", C.c_int, C.POINTER(_UC), C.c_uint64, C.c_uint64, C.POINTER(_GV))
 _sig("gl_micro_records", C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p)
+_sig("gl_edge_motif_records", C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p)
 _sig("gl_edge_counts", C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p)
 _sig("gl_edge_counts_device", C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
      C.POINTER(C.c_void_p))
@@ -403,6 +407,22 @@ class Graph:
         _check(LIB.gl_micro_records(self._h, first, count, out.ctypes.data_as(C.c_void_p)))
         return out
 
+    def edge_motif_records(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        """EdgeMotifRecord rows (t, s_u, s_v, x7, x10, work_units) of edge ids
+        [first, first+count), identical to the reference's process_edge_hash
+        (kernels.cpp:143-156) including its operation counter."""
+        if count is None:
+            count = self.num_edges() - first
+        if first < 0 or count < 0:
+            raise ValueError("negative edge range")
+        out = np.zeros(count, dtype=MOTIF_DTYPE)
+        _check(LIB.gl_edge_motif_records(self._h, first, count, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def process_edge_hash(self, edge_id: int) -> np.void:
+        """kernels.cpp:143-156 for one oriented edge id (after count())."""
+        return self.edge_motif_records(edge_id, 1)[0]
+
     def edge_counts(self, first: int = 0, count: int | None = None, t=None, x7=None, x10=None):
         if count is None:
             count = self.num_edges() - first
@@ -431,6 +451,15 @@ class Graph:
         t, a, b = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _check(LIB.gl_edge_counts_device(self._h, C.byref(t), C.byref(a), C.byref(b)))
         return t.value, a.value, b.value
+
+
+def local_three_counts(rec, n: int):
+    """counts.cpp:113-120: (x3, x4, x5) of one EdgeMotifRecord / MicroRecord row;
+    std::invalid_argument (InvalidArgument here) when n < 2."""
+    if n < 2:
+        raise InvalidArgument(-1, "local_three_counts needs n >= 2")
+    t, su, sv = int(rec["t"]), int(rec["s_u"]), int(rec["s_v"])
+    return t, su + sv, n - (su + sv + t) - 2
 
 
 def version() -> str:

@@ -326,6 +326,15 @@ int gl_micro_records(const gl_graph* g, uint64_t first, uint64_t count, gl_micro
     });
 }
 
+int gl_edge_motif_records(const gl_graph* g, uint64_t first, uint64_t count, gl_edge_motif_record* out) {
+    return guarded([&] {
+        auto& gr = G(g);
+        if (!out && count) throw gl::invalid_argument("null output");
+        static_assert(sizeof(gl_edge_motif_record) == 5 * sizeof(uint64_t), "record layout");
+        gl::edge_motif_records(gr, first, count, reinterpret_cast<gl::u64*>(out));
+    });
+}
+
 int gl_edge_counts(const gl_graph* g, uint64_t first, uint64_t count, uint32_t* t, uint64_t* x7,
                    uint64_t* x10) {
     return guarded([&] {

@@ -511,6 +511,12 @@ void dev_sort_desc(DevBuf& tmp, u32* keys_in, u32* keys_out, u32* ids_in, u32* i
                                                       (int64_t)n, 0, (int)kKeyBits, s));
 }
 
+// Dynamic shared memory of a block H-pass launch: the class's workspace at its
+// largest k, or -- for the xl class when some k exceeds it -- every byte the
+// block can opt into (the small arrays of bigger k plus the phase-2 row stage,
+// hpass_vertex rows_g), minus the kernel's static shared memory.
+template <int MODE, int K> size_t hpass_smem_bytes(u32 kmax, int device);
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size)
 template <typename K> void smem_attr(K* kernel, size_t smem, int device) {
     static std::mutex mu;
@@ -518,6 +524,24 @@ template <typename K> void smem_attr(K* kernel, size_t smem, int device) {
     std::lock_guard<std::mutex> lk(mu);
     if (done.insert({reinterpret_cast<const void*>(kernel), device, smem}).second)
         GL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+template <int MODE, int K> size_t hpass_smem_bytes(u32 kmax, int device) {
+    const u32 kws = K == 1088 ? 1088u : (K == 768 ? 512u : 128u); // largest k of the class
+    const size_t base = (size_t)hpass_ws_words(kws, MODE, bloom_words<HCfg<K>::BLOG>()) * sizeof(u32);
+    if (K != 1088 || kmax <= 1088u) return base;
+    static std::mutex mu;
+    static size_t cached[2][64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& c = cached[MODE][device & 63];
+    if (!c) {
+        cudaFuncAttributes fa{};
+        GL_CUDA(cudaFuncGetAttributes(&fa, k_hpass_block<MODE, K>));
+        int optin = 0;
+        GL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        c = ((size_t)optin - fa.sharedSizeBytes) & ~(size_t)15;
+    }
+    return std::max(base, c);
 }
 
 template <typename T> T read_dev(const T* p, cudaStream_t s) {
@@ -663,6 +687,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const u32 kmax = (u32)(hc[14] & 0xffffffffu);
                 if (kmax >= 65536u) throw overflow_error("|U(a)| >= 65536: H-edge packing needs 16-bit member ids");
                 cs.h_gstride = 0;
+                cs.h_kmax = kmax;
                 if (kmax > 1088u) { // beyond the xl shared-memory workspace: per-block global scratch
                     cs.h_gstride = (hpass_ws_words(kmax, kHPassCount, bloom_words<HCfg<1088>::BLOG>()) + 1) & ~1ull;
                     cs.scratch.alloc((u64)sms * HCfg<1088>::MINB * cs.h_gstride * sizeof(u32));
@@ -679,16 +704,14 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     constexpr int K = decltype(kc)::value;
                     k_take_rank<u32><<<grid1d(count, 256, sms), 256, 0, s>>>(iout, offset, total, rank, world, list);
                     GL_LAUNCH_CHECK();
-                    const u32 kws = K == 1088 ? 1088u : (K == 768 ? 512u : 128u); // largest k of the class
-                    const size_t smem =
-                        (size_t)hpass_ws_words(kws, kHPassCount, bloom_words<HCfg<K>::BLOG>()) * sizeof(u32);
+                    const size_t smem = hpass_smem_bytes<kHPassCount, K>(kmax, gr.device);
                     smem_attr(k_hpass_block<kHPassCount, K>, smem, gr.device);
                     const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hbase,
                                      cs.tl_n.as<u32>() + hbase};
                     const bool glob = K == 1088 && cs.h_gstride;
                     k_hpass_block<kHPassCount, K><<<(unsigned)sms * HCfg<K>::MINB, HCfg<K>::THREADS, smem, s>>>(
                         g, list, count, queue, cs.t.as<u32>(), d_partials, glob ? cs.scratch.as<u32>() : nullptr,
-                        glob ? cs.h_gstride : 0, cs.hlist.as<uint2>(), hcap, TL);
+                        glob ? cs.h_gstride : 0, cs.hlist.as<uint2>(), hcap, TL, (u32)(smem / sizeof(u32)));
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };
@@ -881,15 +904,14 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40;
     auto sums = [&](auto kc, u64 count, const u32* list, u64 hbase, unsigned long long* queue) {
         constexpr int K = decltype(kc)::value;
-        const u32 kws = K == 1088 ? 1088u : (K == 768 ? 512u : 128u);
-        const size_t smem = (size_t)hpass_ws_words(kws, kHPassSums, bloom_words<HCfg<K>::BLOG>()) * sizeof(u32);
+        const size_t smem = hpass_smem_bytes<kHPassSums, K>(cs.h_kmax, gr.device);
         smem_attr(k_hpass_block<kHPassSums, K>, smem, gr.device);
         const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hbase,
                          cs.tl_n.as<u32>() + hbase};
         const bool glob = K == 1088 && cs.h_gstride;
         k_hpass_block<kHPassSums, K><<<(unsigned)sms * HCfg<K>::MINB, HCfg<K>::THREADS, smem, s>>>(
             g, list, count, queue, cs.t.as<u32>(), d_partials, glob ? cs.scratch.as<u32>() : nullptr,
-            glob ? cs.h_gstride : 0, nullptr, 0, TL);
+            glob ? cs.h_gstride : 0, nullptr, 0, TL, (u32)(smem / sizeof(u32)));
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     };
@@ -989,7 +1011,59 @@ __global__ void k_micro(DevGraph g, const u32* __restrict__ t, const u64* __rest
         o[9] = de;
     }
 }
+
+// sum of neighbour degrees per vertex (one warp per vertex)
+__global__ void k_nbr_degree_sum(DevGraph g, u64* __restrict__ out) {
+    const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nwarp = ((u64)gridDim.x * blockDim.x) >> 5;
+    for (u64 v = warp; v < g.n; v += nwarp) {
+        u64 s = 0;
+        for (u64 p = g.off[v] + lane_id(); p < g.off[v + 1]; p += 32) s += g.deg[g.adj[p]];
+        s = warp_sum_u64(s);
+        if (lane_id() == 0) out[v] = s;
+    }
+}
+// EdgeMotifRecord rows {edge_id | t << 32, s_u | s_v << 32, x7, x10, work_units}
+__global__ void k_motif(DevGraph g, const u32* __restrict__ t, const u64* __restrict__ x7,
+                        const u64* __restrict__ x10, const u64* __restrict__ nbrsum, u64 first, u64 count,
+                        u64* __restrict__ out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
+        const u64 e = first + i;
+        const u32 u = g.eu[e], v = g.ev[e];
+        const u64 te = t[e], du = g.deg[u], dv = g.deg[v];
+        u64* o = out + 5 * i;
+        o[0] = e | (te << 32);
+        o[1] = (du - te - 1) | ((dv - te - 1) << 32);
+        o[2] = x7[e];
+        o[3] = x10[e];
+        o[4] = du + dv + nbrsum[u];
+    }
+}
 } // namespace
+
+void edge_motif_records(const Graph& gr, u64 first, u64 count, u64* host_out) {
+    GL_CUDA(cudaSetDevice(gr.device));
+    const CountState& cs = gr.cs;
+    if (!cs.have_micro) throw state_error("no counts computed yet");
+    if (first < cs.shard_begin || first > cs.shard_end || count > cs.shard_end - first)
+        throw invalid_argument("edge range outside the computed shard");
+    if (count == 0) return;
+    cudaStream_t s = gr.stream;
+    const int sms = num_sms(gr.device);
+    DevBuf nbr, tmp;
+    nbr.alloc((gr.d.n + 1) * sizeof(u64));
+    k_nbr_degree_sum<<<grid1d(gr.d.n * 32, 256, sms), 256, 0, s>>>(gr.d, nbr.as<u64>());
+    GL_LAUNCH_CHECK();
+    const u64 chunk = 1ull << 22;
+    tmp.alloc(std::min(count, chunk) * 5 * sizeof(u64));
+    for (u64 off = 0; off < count; off += chunk) {
+        const u64 c = std::min(chunk, count - off);
+        k_motif<<<grid1d(c, 256, sms), 256, 0, s>>>(gr.d, cs.t.as<u32>(), cs.x7.as<u64>(), cs.x10.as<u64>(),
+                                                    nbr.as<u64>(), first + off, c, tmp.as<u64>());
+        GL_LAUNCH_CHECK();
+        GL_CUDA(cudaMemcpyAsync(host_out + 5 * off, tmp.p, c * 5 * sizeof(u64), cudaMemcpyDeviceToHost, s));
+        GL_CUDA(cudaStreamSynchronize(s)); // tmp is reused by the next chunk
+    }
+}
 
 void micro_records(const Graph& gr, u64 first, u64 count, u64* host_out) {
     GL_CUDA(cudaSetDevice(gr.device));

@@ -95,6 +95,7 @@ struct CountState {
     bool mid_done = false;
     int rank = 0, world = 1;
     u64 s1 = 0, h_gstride = 0; // H-pass streamed entries, global workspace stride
+    u32 h_kmax = 0;            // largest |U(a)| of the last count
     float ms[5] = {0, 0, 0, 0, 0};
     u32 launches = 0;
     u64 work[4] = {0, 0, 0, 0};
@@ -133,6 +134,7 @@ void count_mid(Graph& g, i64* d_partials, cudaStream_t s);
 void count_finish(Graph& g, const i64* d_partials, u64 begin, u64 end, u128 C[17],
                   cudaStream_t s);
 void micro_records(const Graph& g, u64 first, u64 count, u64* host_out /* count*10 */);
+void edge_motif_records(const Graph& g, u64 first, u64 count, u64* host_out /* count*5 */);
 
 // algebra.cpp
 void global_from_unrestricted(const u128 C[17], u64 n, u64 m, u128 X[18]);

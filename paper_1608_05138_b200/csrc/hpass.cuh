@@ -71,6 +71,16 @@ __host__ __device__ inline u64 hpass_ws_words(u32 k, int mode, u32 bloom_w) {
     return body + 2 + H + H / 2 + bloom_w + 2ull * k; // + member list bounds
 }
 
+// the counting workspace without the bitmap rows (xs, tri, hash, Bloom, member
+// bounds): kept in shared memory for k beyond the class KMAX while the rows go
+// to the block's global scratch (hpass_vertex rows_g)
+__host__ __device__ inline u64 hpass_small_words(u32 k, u32 bloom_w) {
+    u32 l = 6;
+    while ((1u << l) < 2 * k) ++l;
+    const u64 H = 1ull << l;
+    return 2ull * k + 2 + H + H / 2 + bloom_w + 2ull * k;
+}
+
 __device__ __forceinline__ void atomic_add_i64(i64* p, i64 v) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
@@ -390,10 +400,15 @@ __device__ u64 block_exclusive_scan64(u64* a, u32 n) {
 // shared memory (k <= the class KMAX: every workspace access compiles to LDS/STS/
 // ATOMS) or the block's global scratch (larger k).
 
+// rows_g (kHPassCount, k beyond the shared workspace): the bitmap rows live in
+// global scratch, everything else in ws (shared); phase 2 then stages column
+// chunks of all rows into the stage_words of shared memory left after the
+// small arrays and adds each chunk's popcounts (t once, x7 per chunk).
 template <int MODE, int BLOG, typename Cand>
 __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
                                              Cand* cbuf, uint2* hlist, u32& s_nh, u32& s_mi, u32 a, u64 ub, u32 k,
-                                             u32 W, u32 hl, u32 H, const TriList& TL, u64 idx, u64& s_base) {
+                                             u32 W, u32 hl, u32 H, const TriList& TL, u64 idx, u64& s_base,
+                                             u32* rows_g = nullptr, u32 stage_words = 0) {
     const u32 lane = lane_id();
     if (MODE == kHPassSums && TL.rec && TL.base[idx] != kNoList) {
         // stream this vertex's H-edge records: t of (x_i, x_j) gathered, the
@@ -435,11 +450,11 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     }
     u32* xs = ws;
     u32* tri = xs + k;                      // kHPassCount
-    u32* rows = tri + k;                    // kHPassCount
+    u32* rows = rows_g ? rows_g : tri + k;  // kHPassCount
     u32* ta = xs + k;                       // kHPassSums
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
     const u32 RS = hrow_stride(k), W2 = (k + 63u) >> 6; // u32 stride, u64 words per row
-    const u64 body = MODE == kHPassCount ? 2ull * k + (u64)k * RS : ((2ull * k + 1) & ~1ull) + 2ull * k;
+    const u64 body = MODE == kHPassCount ? 2ull * k + (rows_g ? 0ull : (u64)k * RS) : ((2ull * k + 1) & ~1ull) + 2ull * k;
     u32* bloom = ws + body;
     u32* hkey = bloom + bloom_words<BLOG>();
     unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
@@ -608,7 +623,51 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         }
     }
     __syncthreads();
-    if (MODE == kHPassCount) {
+    if (MODE == kHPassCount && rows_g) {
+        // phase 2 with the rows in global scratch: column chunks of every row
+        // staged in shared memory (odd u64 stride), one sweep of the H-edge
+        // list per chunk
+        const u32 nh = s_nh;
+        if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
+        unsigned long long* st =
+            reinterpret_cast<unsigned long long*>(me + k + ((uintptr_t)(me + k) & 4u ? 1 : 0)); // 8 B aligned
+        u32 cw = stage_words / (2u * k) - 1u; // u64 words per row per chunk (stride cw | 1 <= cw + 1)
+        cw = cw < 1u ? 1u : (cw > W2 ? W2 : cw);
+        const u32 sst = cw | 1u;
+        const unsigned long long* R = reinterpret_cast<const unsigned long long*>(rows);
+        const u32 RS2 = RS >> 1;
+        for (u32 c0 = 0; c0 < W2; c0 += cw) {
+            const u32 nw = W2 - c0 < cw ? W2 - c0 : cw;
+            for (u32 q = threadIdx.x; q < k * nw; q += blockDim.x) {
+                const u32 i = q / nw, v = q - i * nw;
+                st[(u64)i * sst + v] = R[(u64)i * RS2 + c0 + v];
+            }
+            __syncthreads();
+            for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
+                const uint2 he = hout[h];
+                const u32 i = he.x & 0xffffu, j = he.x >> 16;
+                const unsigned long long* ri = st + (u64)i * sst;
+                const unsigned long long* rj = st + (u64)j * sst;
+                u32 c = 0;
+                for (u32 v = 0; v < nw; ++v) c += __popcll(ri[v] & rj[v]);
+                if (c0 == 0) atomicAdd(&t[he.y], 1u);
+                if (c) {
+                    atomicAdd(&tri[i], c);
+                    atomicAdd(&tri[j], c);
+                    atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
+                }
+            }
+            __syncthreads();
+        }
+        // phase 3: edges (a, x_i)
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+            u32 deg = 0;
+            for (u32 v = 0; v < W2; ++v) deg += __popcll(R[(u64)i * RS2 + v]);
+            const u32 e = g.eid[ub + i];
+            if (deg) atomicAdd(&t[e], deg);
+            if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
+        }
+    } else if (MODE == kHPassCount) {
         // phase 2: stream the H-edges (kept in the device-wide list when it had room)
         const u32 nh = s_nh;
         if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
@@ -649,7 +708,7 @@ template <int MODE, int KMAX>
 __global__ void __launch_bounds__(HCfg<KMAX>::THREADS, HCfg<KMAX>::MINB)
 k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned long long* __restrict__ queue,
               u32* __restrict__ t, i64* __restrict__ part, u32* __restrict__ gscratch, u64 gstride,
-              uint2* __restrict__ hlist_all, u64 hcap, TriList TL) {
+              uint2* __restrict__ hlist_all, u64 hcap, TriList TL, u32 smem_words) {
     constexpr int BLOG = HCfg<KMAX>::BLOG;
     extern __shared__ u32 smem[];
     __shared__ unsigned long long s_idx;
@@ -680,14 +739,21 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         const u32 k = (u32)(g.off[a + 1] - ub);
         const u32 W = (k + 31) >> 5;
         const u32 hl = hp_log(k), H = 1u << hl;
-        if (MODE == kHPassSums) // one generic-pointer copy measured faster for the lighter sums pass
-            hpass_vertex<MODE, BLOG>(g, t, part, k <= (u32)KMAX ? smem : gscratch + (u64)blockIdx.x * gstride,
-                                     cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
-        else if (k <= (u32)KMAX)
+        if (MODE == kHPassSums) { // one generic-pointer copy measured faster for the lighter sums pass
+            const bool sm = hpass_ws_words(k, kHPassSums, bloom_words<BLOG>()) <= smem_words;
+            hpass_vertex<MODE, BLOG>(g, t, part, sm ? smem : gscratch + (u64)blockIdx.x * gstride, cbuf, hlist,
+                                     s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
+        } else if (k <= (u32)KMAX) {
             hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
-        else
+        } else if (hpass_small_words(k, bloom_words<BLOG>()) + 6ull * k <= smem_words) {
+            // rows in global scratch, the rest (and the phase-2 chunk stage) in shared memory
+            const u32 small = (u32)hpass_small_words(k, bloom_words<BLOG>());
+            hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base,
+                                     gscratch + (u64)blockIdx.x * gstride, smem_words - small - 2);
+        } else {
             hpass_vertex<MODE, BLOG>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a,
                                      ub, k, W, hl, H, TL, idx, s_base);
+        }
     }
 }
 

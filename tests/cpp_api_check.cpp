@@ -38,6 +38,17 @@ int main() {
     assert(inconsistent);
     assert(std::string(gb::graphlet_name(10)) == "4-cycle" && std::string(gb::graphlet_name(0)) == "?");
     assert(gb::to_decimal((gb::count_t)1 << 100) == "1267650600228229401496703205376");
+    // counts.cpp:113-120
+    gb::EdgeMotifRecord rec{0, 2, 3, 1, 1, 0, 0};
+    const gb::LocalThree l3 = gb::local_three_counts(rec, 10);
+    assert(l3.x3 == 2 && l3.x4 == 4 && l3.x5 == 2);
+    bool small = false;
+    try {
+        gb::local_three_counts(rec, 1);
+    } catch (const std::invalid_argument&) {
+        small = true;
+    }
+    assert(small);
     std::printf("ok\n");
     return 0;
 }

@@ -98,3 +98,41 @@ def test_count_sharded_world1_on_default_stream(cuda_device):
     p = torch.empty(2 * g.partials_len(1), dtype=torch.int64, device="cuda")
     with pytest.raises(ValueError, match="stream"):
         sharded_step(g, p, 0, 1, torch.cuda.default_stream())
+
+
+def test_cpp_mirror_on_device(cuda_device, tmp_path):
+    """include/graphlet_b200.hpp on the device: graph.hpp:56-79 accessors and
+    process_edge_hash records (tests/cpp_gpu_check.cpp)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "cpp_gpu_check"
+    libdir = os.path.dirname(gl.lib_path())
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp_gpu_check.cpp"), "-o", str(exe), "-L", libdir,
+                    "-lgraphlet_b200", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "ok"
+
+
+def test_edge_motif_records_match_reference_pipeline(cuda_device):
+    """EdgeMotifRecord rows (t, s_u, s_v, x7, x10, work_units) equal the
+    reference's own process_edge_hash records (oracle/_ref: the reference's
+    sources compiled in place) on RMAT / BA graphs."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import oracle as O
+    for pairs in (gl.generate_rmat(10, 8, seed=3), gl.generate_ba(3000, 5, seed=2)):
+        g = gl.Graph.build(pairs, cuda_device)
+        g.count()
+        rec = g.edge_motif_records()
+        if not O.ref_available():
+            pytest.skip("oracle/_ref not built (it ships with the snapshot from the build container)")
+        ref = O.RefLib(pairs).edge_records(0)
+        got = np.stack([rec[f].astype(np.uint64) for f in ("t", "s_u", "s_v", "x7", "x10", "work_units")], 1)
+        assert np.array_equal(got, ref)
+        assert np.array_equal(rec["edge_id"], np.arange(g.num_edges(), dtype=np.uint32))
+        one = g.process_edge_hash(7)
+        assert tuple(int(one[f]) for f in ("t", "x7", "x10", "work_units")) == tuple(int(x) for x in ref[7, [0, 3, 4, 5]])
+        assert gl.local_three_counts(one, g.num_vertices())[0] == int(one["t"])

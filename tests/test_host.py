@@ -143,7 +143,7 @@ def test_cpp_api_mirror_host_calls(tmp_path):
     against the product library; its host-only calls behave like the reference."""
     exe = tmp_path / "cpp_api_check"
     libdir = os.path.dirname(gl.lib_path())
-    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp_api_check.cpp"), "-o", str(exe), "-L", libdir,
                     "-lgraphlet_b200", f"-Wl,-rpath,{libdir}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout

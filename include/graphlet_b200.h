@@ -69,6 +69,11 @@ typedef struct {
 int gl_load_edge_list(const char *text, size_t len, uint64_t **pairs, uint64_t *count);
 /* load_edge_list_file (graph.hpp:39; graph.cpp:87-91). */
 int gl_load_edge_list_file(const char *path, uint64_t **pairs, uint64_t *count);
+/* load_edge_list (graph.cpp:47-85) executed on `device`: the text is copied to
+ * HBM and cut, checked and parsed there, one thread per line (same rules and
+ * the same parse_error line numbers and messages as gl_load_edge_list).
+ * Pairs returned like gl_load_edge_list (free with gl_free). */
+int gl_parse_edge_list_device(const char *text, size_t len, int device, uint64_t **pairs, uint64_t *count);
 void gl_free(void *p);
 /* Device memory freed by gl_graph_free is cached per device for the next
  * graph (no reference counterpart: the reference is host-only); this returns
@@ -100,6 +105,9 @@ typedef struct gl_graph gl_graph; /* device-resident preprocessed graph */
 int gl_graph_build(const uint64_t *pairs, uint64_t count, int device, gl_graph **out);
 /* Same, `d_pairs` already in device memory on `device` (not modified). */
 int gl_graph_build_device(const uint64_t *d_pairs, uint64_t count, int device, gl_graph **out);
+/* gl_parse_edge_list_device + build_graph without the pairs leaving the device:
+ * edge-list text -> device-resident graph. */
+int gl_graph_build_text(const char *text, size_t len, int device, gl_graph **out);
 void gl_graph_free(gl_graph *g);
 
 uint64_t gl_graph_num_vertices(const gl_graph *g); /* Graph::num_vertices */

@@ -29,7 +29,7 @@ import numpy as np
 
 __all__ = [
     "GraphletError", "ParseError", "CountConsistencyError", "CountOverflowError",
-    "CudaError", "Graph", "load_edge_list", "load_edge_list_file", "generate_rmat",
+    "CudaError", "Graph", "load_edge_list", "load_edge_list_file", "parse_edge_list_device", "generate_rmat",
     "generate_rmat_device", "generate_gnm", "generate_ba", "global_from_unrestricted",
     "graphlet_name", "GRAPHLET_NAMES", "MICRO_DTYPE", "MOTIF_DTYPE", "local_three_counts", "lib_path", "LIB",
 ]
@@ -98,6 +98,8 @@ _sig("gl_version", C.c_char_p)
 _sig("gl_free", None, C.c_void_p)
 _sig("gl_load_edge_list", C.c_int, C.c_char_p, C.c_size_t, C.POINTER(_u64p), _u64p)
 _sig("gl_load_edge_list_file", C.c_int, C.c_char_p, C.POINTER(_u64p), _u64p)
+_sig("gl_parse_edge_list_device", C.c_int, C.c_char_p, C.c_size_t, C.c_int, C.POINTER(_u64p), _u64p)
+_sig("gl_graph_build_text", C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.POINTER(C.c_void_p))
 _sig("gl_generate_rmat", C.c_int, C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
      C.c_uint64, C.POINTER(_u64p), _u64p)
 _sig("gl_generate_rmat_device", C.c_int, C.c_uint32, C.c_uint32, C.c_double, C.c_double,
@@ -203,6 +205,16 @@ def load_edge_list(text) -> np.ndarray:
     return _take_pairs(ptr, cnt)
 
 
+def parse_edge_list_device(text, device: int = 0) -> np.ndarray:
+    """load_edge_list (graph.cpp:47-85) executed on the GPU (parse.cu): same
+    pairs, same ParseError line numbers and messages as load_edge_list."""
+    if isinstance(text, str):
+        text = text.encode()
+    ptr, cnt = _u64p(), C.c_uint64()
+    _check(LIB.gl_parse_edge_list_device(text, len(text), device, C.byref(ptr), C.byref(cnt)))
+    return _take_pairs(ptr, cnt)
+
+
 def load_edge_list_file(path: str) -> np.ndarray:
     ptr, cnt = _u64p(), C.c_uint64()
     _check(LIB.gl_load_edge_list_file(os.fsencode(path), C.byref(ptr), C.byref(cnt)))
@@ -286,6 +298,20 @@ class Graph:
         """gl_graph_build on a raw (e.g. pinned) host pointer of 2*count labels."""
         h = C.c_void_p()
         _check(LIB.gl_graph_build(C.c_void_p(host_ptr), count, device, C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def build_text(cls, text, device: int = 0) -> "Graph":
+        """Edge-list text (bytes / str, or a host pointer + length tuple) ->
+        graph, parsed on the device (gl_graph_build_text)."""
+        h = C.c_void_p()
+        if isinstance(text, tuple):
+            ptr, n = text
+            _check(LIB.gl_graph_build_text(C.c_void_p(ptr), n, device, C.byref(h)))
+        else:
+            if isinstance(text, str):
+                text = text.encode()
+            _check(LIB.gl_graph_build_text(text, len(text), device, C.byref(h)))
         return cls(h.value, device)
 
     @classmethod

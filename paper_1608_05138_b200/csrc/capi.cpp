@@ -136,6 +136,37 @@ int gl_load_edge_list_file(const char* path, uint64_t** pairs, uint64_t* count) 
     });
 }
 
+int gl_parse_edge_list_device(const char* text, size_t len, int device, uint64_t** pairs, uint64_t* count) {
+    return guarded([&] {
+        if (!text && len) throw gl::invalid_argument("null text");
+        require_device(device);
+        gl::DevBuf d;
+        const gl::u64 k = gl::parse_edge_list_device(text, len, device, d, nullptr);
+        std::vector<gl::u64> host(2 * k);
+        if (k) GL_CUDA(cudaMemcpy(host.data(), d.p, 2 * k * sizeof(gl::u64), cudaMemcpyDeviceToHost));
+        export_pairs(std::move(host), pairs, count);
+    });
+}
+
+int gl_graph_build_text(const char* text, size_t len, int device, gl_graph** out) {
+    return guarded([&] {
+        if (!out) throw gl::invalid_argument("null output pointer");
+        if (!text && len) throw gl::invalid_argument("null text");
+        require_device(device);
+        gl::DevBuf d;
+        const gl::u64 k = gl::parse_edge_list_device(text, len, device, d, nullptr);
+        if (!k) d.alloc(16);
+        auto* h = new gl_graph;
+        try {
+            h->g = gl::build_graph_device(d.as<gl::u64>(), k, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
 int gl_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c, uint64_t seed,
                      uint64_t** pairs, uint64_t* count) {
     return guarded([&] {

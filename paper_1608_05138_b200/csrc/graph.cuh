@@ -127,6 +127,9 @@ struct Graph {
 Graph* build_graph_device(const u64* d_pairs, u64 count, int device);
 void generate_rmat_device(const RmatParams& p, u64 count, u64* d_pairs, cudaStream_t s);
 
+// parse.cu
+u64 parse_edge_list_device(const char* host_text, u64 len, int device, DevBuf& d_pairs, cudaStream_t s);
+
 // count.cu
 extern std::atomic<int> g_overlap;
 void count_begin(Graph& g, int rank, int world, i64* d_partials, cudaStream_t s);

@@ -165,6 +165,36 @@ std::vector<u64> parse_edge_list(const char* text, size_t len) {
     return out;
 }
 
+// The reference's error for one data line (its own text, no '\n'), numbered
+// line_no: the device parser (parse.cu) locates the first bad line, this
+// formats exactly the message the scanner above would have thrown there.
+void throw_line_error(const char* line, size_t len, u64 line_no) {
+    const char* b = line;
+    const char* e = line + len;
+    const char* tok[2][2] = {};
+    int nt = 0;
+    const char* p = b;
+    while (p < e) {
+        while (p < e && is_sep(*p)) ++p;
+        if (p >= e) break;
+        const char* q = p;
+        while (q < e && !is_sep(*q)) ++q;
+        if (nt < 2) {
+            tok[nt][0] = p;
+            tok[nt][1] = q;
+        }
+        ++nt;
+        p = q;
+    }
+    if (nt != 2) throw parse_error(line_no, "expected two integer tokens, got " + std::to_string(nt));
+    u64 x;
+    if (!parse_u64(tok[0][0], tok[0][1], x))
+        throw parse_error(line_no, "malformed token '" + std::string(tok[0][0], tok[0][1]) + "'");
+    if (!parse_u64(tok[1][0], tok[1][1], x))
+        throw parse_error(line_no, "malformed token '" + std::string(tok[1][0], tok[1][1]) + "'");
+    throw parse_error(line_no, "malformed line");
+}
+
 std::vector<u64> parse_edge_list_file(const std::string& path) {
     std::ifstream in(path, std::ios::binary);
     if (!in) throw io_error("cannot open '" + path + "'");

@@ -57,6 +57,7 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-text-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--e2e-warmup", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -390,6 +391,49 @@ def run_ours(args):
                    "ms_per_step": tot_rec / max(1, len(rec_ms)),
                    "includes": "same step ending in the full 80-byte MicroRecord table (micro_counts, "
                                "counts.cpp:122-136) of every edge, D2H into pinned memory"}}
+
+    # ---- e2e from an edge-list TEXT (load_edge_list, graph.cpp:47-85): the
+    # same step starting from the file bytes in pinned host memory, parsed on
+    # the device (gl_graph_build_text) -- and, once, parsed by the host scanner
+    # (gl_load_edge_list + gl_graph_build) for comparison.  World 1, m <= 2^25
+    # (the text is formatted in Python once, outside the timed region).
+    if e2e is not None and world == 1 and m <= (1 << 25) and not args.no_text_e2e:
+        hp2 = hp if hp is not None else host_pairs(args)
+        txt = ("\n".join(f"{a} {c}" for a, c in hp2.tolist()) + "\n").encode()
+        pin_txt = torch.frombuffer(bytearray(txt), dtype=torch.uint8).pin_memory()
+        tms = []
+        for i in range(args.e2e_steps + args.e2e_warmup):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g4 = gl.Graph.build_text((pin_txt.data_ptr(), pin_txt.numel()), local)  # gl_graph_build_text
+            p4 = torch.empty(2 * g4.partials_len(1), dtype=torch.int64, device=dev)
+            X4, _ = sharded_step(g4, p4, 0, 1, stream)
+            g4.edge_counts(0, m, pin_t.numpy().view(np.uint32)[:m], pin_x7.numpy().view(np.uint64)[:m],
+                           pin_x10.numpy().view(np.uint64)[:m])
+            dt = (time.perf_counter() - t0) * 1e3
+            g4.close()
+            del p4
+            assert X4 == X, "text e2e counts differ"
+            if i >= args.e2e_warmup:
+                tms.append(dt)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g5 = gl.Graph.build(gl.load_edge_list(txt), local)  # host scanner + gl_graph_build
+        p5 = torch.empty(2 * g5.partials_len(1), dtype=torch.int64, device=dev)
+        X5, _ = sharded_step(g5, p5, 0, 1, stream)
+        g5.edge_counts(0, m, pin_t.numpy().view(np.uint32)[:m], pin_x7.numpy().view(np.uint64)[:m],
+                       pin_x10.numpy().view(np.uint64)[:m])
+        host_ms = (time.perf_counter() - t0) * 1e3
+        g5.close()
+        assert X5 == X
+        e2e["from_text"] = {
+            "value": m * len(tms) / (sum(tms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": len(txt),
+            "d2h_bytes_per_step": int(m * (4 + 8 + 8) + 18 * 16), "ms_per_step": sum(tms) / len(tms),
+            "includes": "H2D of the edge-list text (pinned), load_edge_list rules on the device (parse.cu), "
+                        "CSR build, count, D2H of t/x7/x10 + X",
+            "host_parser_ms_per_step": host_ms,
+            "host_parser_note": "same step with the text parsed by the host scanner (gl_load_edge_list, one "
+                                "thread) and the pairs copied from pageable memory; one step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

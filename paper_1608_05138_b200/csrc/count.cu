@@ -578,6 +578,12 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     const u64 m = g.m, n = g.n;
     // adjacency slots are carried as u32 in the cycle run metadata
     if (2 * m >= (1ull << 32)) throw overflow_error("counting needs 2m < 2^32 adjacency slots (m < 2^31 edges)");
+    {
+        // dense cycle windows count their runs in 24 bits (runs <= |L(a)| <= max degree)
+        const char* e = std::getenv("GL_TEST_DEGREE_LIMIT"); // tests reach this path on small graphs
+        const u64 lim = e && *e ? std::strtoull(e, nullptr, 10) : (1ull << 24);
+        if (g.dmax >= lim) throw overflow_error("cycle pass needs max degree < 2^24 (window run counts)");
+    }
     // A cycle pass of a previous count_begin that was never joined by
     // count_mid is still writing the slot accumulators and reading the queue
     // counters: finish it before any of them is reset below.
@@ -587,6 +593,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     // partials that the memsets below reset
     if (cs.began) {
         GL_CUDA(cudaEventSynchronize(cs.ev[1]));
+        GL_CUDA(cudaEventSynchronize(cs.ev[3])); // cycle pass (on the previous caller stream when serialised)
         if (cs.mid_done) GL_CUDA(cudaEventSynchronize(cs.ev[7]));
     }
     cs.launches = 0;
@@ -808,11 +815,6 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* lsmall = lsmid + mysmid;
             if (mysparse_p || mybig_p || mymid || mysmid) {
                 if (2 * m >= (1ull << 32)) throw overflow_error("cycle pass needs 2m < 2^32 adjacency slots");
-                {
-                    const char* e = std::getenv("GL_TEST_DEGREE_LIMIT"); // tests reach this path on small graphs
-                    const u64 lim = e && *e ? std::strtoull(e, nullptr, 10) : (1ull << 24);
-                    if (g.dmax >= lim) throw overflow_error("cycle pass needs max degree < 2^24 (window run counts)");
-                }
                 // per-block scratch: big tops need dmax + 2 entries, hash tops at most
                 // their wedge bound (nb <= wedges)
                 const u32 cap_big = (g.dmax + 3) & ~1u;

@@ -400,15 +400,16 @@ __device__ u64 block_exclusive_scan64(u64* a, u32 n) {
 // shared memory (k <= the class KMAX: every workspace access compiles to LDS/STS/
 // ATOMS) or the block's global scratch (larger k).
 
-// rows_g (kHPassCount, k beyond the shared workspace): the bitmap rows live in
-// global scratch, everything else in ws (shared); phase 2 then stages column
-// chunks of all rows into the stage_words of shared memory left after the
-// small arrays and adds each chunk's popcounts (t once, x7 per chunk).
+// big (kHPassCount, k beyond the shared workspace): no bitmap is built in
+// phase 1 (only the H-edge records); phase 2 rebuilds H_a's rows one column
+// chunk at a time in the stage_words of shared memory left after the small
+// arrays -- every record sets its two bits of the chunk -- and adds each
+// chunk's popcounts (t once, x7 and the member degrees per chunk).
 template <int MODE, int BLOG, typename Cand>
 __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
                                              Cand* cbuf, uint2* hlist, u32& s_nh, u32& s_mi, u32 a, u64 ub, u32 k,
                                              u32 W, u32 hl, u32 H, const TriList& TL, u64 idx, u64& s_base,
-                                             u32* rows_g = nullptr, u32 stage_words = 0) {
+                                             bool big = false, u32 stage_words = 0) {
     const u32 lane = lane_id();
     if (MODE == kHPassSums && TL.rec && TL.base[idx] != kNoList) {
         // stream this vertex's H-edge records: t of (x_i, x_j) gathered, the
@@ -450,11 +451,11 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     }
     u32* xs = ws;
     u32* tri = xs + k;                      // kHPassCount
-    u32* rows = rows_g ? rows_g : tri + k;  // kHPassCount
+    u32* rows = tri + k;                    // kHPassCount (not used when big)
     u32* ta = xs + k;                       // kHPassSums
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws + ((2ull * k + 1) & ~1ull)); // kHPassSums
     const u32 RS = hrow_stride(k), W2 = (k + 63u) >> 6; // u32 stride, u64 words per row
-    const u64 body = MODE == kHPassCount ? 2ull * k + (rows_g ? 0ull : (u64)k * RS) : ((2ull * k + 1) & ~1ull) + 2ull * k;
+    const u64 body = MODE == kHPassCount ? 2ull * k + (big ? 0ull : (u64)k * RS) : ((2ull * k + 1) & ~1ull) + 2ull * k;
     u32* bloom = ws + body;
     u32* hkey = bloom + bloom_words<BLOG>();
     unsigned short* hval = reinterpret_cast<unsigned short*>(hkey + H);
@@ -472,7 +473,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
             acc[i] = 0;
         }
     }
-    if (MODE == kHPassCount)
+    if (MODE == kHPassCount && !big)
         for (u64 w = threadIdx.x; w < (u64)k * RS; w += blockDim.x) rows[w] = 0;
     for (u32 h = threadIdx.x; h < H; h += blockDim.x) hkey[h] = kEmpty;
     for (u32 w = threadIdx.x; w < bloom_words<BLOG>(); w += blockDim.x) bloom[w] = 0;
@@ -512,7 +513,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // one round of (hit, j = member index, e = edge id of (x_i, x_j)) with all lanes
         auto on_hits = [&](bool hit, u32 j, u32 e) {
             if (MODE == kHPassCount) {
-                if (hit) {
+                if (hit && !big) {
                     atomicOr(&rows[(u64)i * RS + (j >> 5)], 1u << (j & 31));
                     atomicOr(&rows[(u64)j * RS + (i >> 5)], 1u << (i & 31));
                 }
@@ -623,24 +624,31 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         }
     }
     __syncthreads();
-    if (MODE == kHPassCount && rows_g) {
-        // phase 2 with the rows in global scratch: column chunks of every row
-        // staged in shared memory (odd u64 stride), one sweep of the H-edge
-        // list per chunk
+    if (MODE == kHPassCount && big) {
+        // phase 2 for big k: per column chunk [64 c0, 64 (c0 + nw)), rebuild
+        // the chunk of every row from the H-edge records (shared 64-bit
+        // atomicOr), then one popcount sweep over the records; member degrees
+        // accumulate per chunk (phase 3)
         const u32 nh = s_nh;
         if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
-        unsigned long long* st =
-            reinterpret_cast<unsigned long long*>(me + k + ((uintptr_t)(me + k) & 4u ? 1 : 0)); // 8 B aligned
-        u32 cw = stage_words / (2u * k) - 1u; // u64 words per row per chunk (stride cw | 1 <= cw + 1)
+        u32* degs = me + k; // u32[k]: member degree in H_a
+        u32* st0 = degs + k;
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(st0 + ((uintptr_t)st0 & 4u ? 1 : 0));
+        const u32 avail = stage_words > k + 2 ? stage_words - k - 2 : 0u; // u32 words left for the stage
+        u32 cw = avail / (2u * k) - 1u;                                    // u64 words per row per chunk
         cw = cw < 1u ? 1u : (cw > W2 ? W2 : cw);
-        const u32 sst = cw | 1u;
-        const unsigned long long* R = reinterpret_cast<const unsigned long long*>(rows);
-        const u32 RS2 = RS >> 1;
+        const u32 sst = cw | 1u;                                           // odd stride: conflict-free rows
+        for (u32 i = threadIdx.x; i < k; i += blockDim.x) degs[i] = 0;
         for (u32 c0 = 0; c0 < W2; c0 += cw) {
             const u32 nw = W2 - c0 < cw ? W2 - c0 : cw;
-            for (u32 q = threadIdx.x; q < k * nw; q += blockDim.x) {
-                const u32 i = q / nw, v = q - i * nw;
-                st[(u64)i * sst + v] = R[(u64)i * RS2 + c0 + v];
+            const u32 lo = c0 * 64u, hi = (c0 + nw) * 64u;
+            for (u32 q = threadIdx.x; q < k * sst; q += blockDim.x) st[q] = 0ull;
+            __syncthreads();
+            for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
+                const uint2 he = hout[h];
+                const u32 i = he.x & 0xffffu, j = he.x >> 16;
+                if (j >= lo && j < hi) atomicOr(&st[(u64)i * sst + ((j - lo) >> 6)], 1ull << (j & 63));
+                if (i >= lo && i < hi) atomicOr(&st[(u64)j * sst + ((i - lo) >> 6)], 1ull << (i & 63));
             }
             __syncthreads();
             for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
@@ -657,14 +665,17 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
                     atomic_add_i64(&part[2 * (u64)he.y], (i64)c);
                 }
             }
+            for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
+                u32 d = 0;
+                for (u32 v = 0; v < nw; ++v) d += __popcll(st[(u64)i * sst + v]);
+                degs[i] += d;
+            }
             __syncthreads();
         }
         // phase 3: edges (a, x_i)
         for (u32 i = threadIdx.x; i < k; i += blockDim.x) {
-            u32 deg = 0;
-            for (u32 v = 0; v < W2; ++v) deg += __popcll(R[(u64)i * RS2 + v]);
             const u32 e = g.eid[ub + i];
-            if (deg) atomicAdd(&t[e], deg);
+            if (degs[i]) atomicAdd(&t[e], degs[i]);
             if (tri[i]) atomic_add_i64(&part[2 * (u64)e], (i64)(tri[i] >> 1));
         }
     } else if (MODE == kHPassCount) {
@@ -745,11 +756,12 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
                                      s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
         } else if (k <= (u32)KMAX) {
             hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base);
-        } else if (hpass_small_words(k, bloom_words<BLOG>()) + 6ull * k <= smem_words) {
-            // rows in global scratch, the rest (and the phase-2 chunk stage) in shared memory
+        } else if (hpass_small_words(k, bloom_words<BLOG>()) + 8ull * k <= smem_words) {
+            // H_a's rows rebuilt per column chunk in shared memory from the
+            // H-edge records (the small arrays, degrees and stage all shared)
             const u32 small = (u32)hpass_small_words(k, bloom_words<BLOG>());
             hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base,
-                                     gscratch + (u64)blockIdx.x * gstride, smem_words - small - 2);
+                                     true, smem_words - small - 2);
         } else {
             hpass_vertex<MODE, BLOG>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a,
                                      ub, k, W, hl, H, TL, idx, s_base);

@@ -631,10 +631,13 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // accumulate per chunk (phase 3)
         const u32 nh = s_nh;
         if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
-        u32* degs = me + k; // u32[k]: member degree in H_a
-        u32* st0 = degs + k;
+        // phase 1's hash, Bloom filter, member ids and list bounds are dead
+        // now: the member degrees take xs' place and the stage everything
+        // after tri (stage_words = the workspace words beyond xs and tri)
+        u32* degs = xs; // u32[k]: member degree in H_a
+        u32* st0 = tri + k;
         unsigned long long* st = reinterpret_cast<unsigned long long*>(st0 + ((uintptr_t)st0 & 4u ? 1 : 0));
-        const u32 avail = stage_words > k + 2 ? stage_words - k - 2 : 0u; // u32 words left for the stage
+        const u32 avail = stage_words > 2 ? stage_words - 2 : 0u;          // u32 words for the stage
         u32 cw = avail / (2u * k) - 1u;                                    // u64 words per row per chunk
         cw = cw < 1u ? 1u : (cw > W2 ? W2 : cw);
         const u32 sst = cw | 1u;                                           // odd stride: conflict-free rows
@@ -759,9 +762,8 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
         } else if (hpass_small_words(k, bloom_words<BLOG>()) + 8ull * k <= smem_words) {
             // H_a's rows rebuilt per column chunk in shared memory from the
             // H-edge records (the small arrays, degrees and stage all shared)
-            const u32 small = (u32)hpass_small_words(k, bloom_words<BLOG>());
             hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base,
-                                     true, smem_words - small - 2);
+                                     true, smem_words - 2 * k);
         } else {
             hpass_vertex<MODE, BLOG>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a,
                                      ub, k, W, hl, H, TL, idx, s_base);

@@ -167,6 +167,12 @@ int gl_global_from_unrestricted(const gl_unrestricted *c, uint64_t n, uint64_t m
 /* micro_counts (counts.hpp:90; counts.cpp:122-136) for edge ids
  * [first, first+count) of the last gl_count / gl_count_finish shard. */
 int gl_micro_records(const gl_graph *g, uint64_t first, uint64_t count, gl_micro_record *out);
+/* gl_count plus the compact per-edge output of every edge id (t, x7, x10, as
+ * gl_edge_counts; any pointer may be NULL): t and x7 are final after the
+ * clique/triangle pass, so their device-to-host copies overlap the cycle pass
+ * (pinned host buffers make that copy truly asynchronous). */
+int gl_count_edges(gl_graph *g, gl_graphlet_vector *X, gl_unrestricted *unres, uint32_t *t, uint64_t *x7,
+                   uint64_t *x10);
 /* EdgeMotifRecord (counts.hpp:20-35) of process_edge_hash (kernels.cpp:143-156)
  * for edge ids [first, first+count) of the last count's shard: t, s_u, s_v,
  * x7, x10 and the reference's deterministic operation counter, which for the

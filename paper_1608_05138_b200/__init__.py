@@ -124,6 +124,7 @@ _sig("gl_triangle_counts_device", C.c_int, C.c_void_p, C.POINTER(C.c_void_p), _u
 _sig("gl_count_finish", C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
      C.POINTER(_UC), C.c_void_p)
 _sig("gl_global_from_unrestricted", C.c_int, C.POINTER(_UC), C.c_uint64, C.c_uint64, C.POINTER(_GV))
+_sig("gl_count_edges", C.c_int, C.c_void_p, C.POINTER(_GV), C.POINTER(_UC), C.c_void_p, C.c_void_p, C.c_void_p)
 _sig("gl_micro_records", C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p)
 _sig("gl_edge_motif_records", C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p)
 _sig("gl_edge_counts", C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -378,6 +379,27 @@ class Graph:
         _check(LIB.gl_count(self._h, C.byref(gv), C.byref(uc)))
         return CountResult([_to_int(gv.x[i]) for i in range(18)], [_to_int(uc.c[i]) for i in range(17)],
                            *self.last_stats())
+
+    def count_edges(self, t=None, x7=None, x10=None):
+        """count() plus every edge's (t, x7, x10) into host arrays (allocated when
+        None; pass pinned numpy views to make the early t/x7 copy asynchronous):
+        t and x7 leave the device while the cycle pass runs (gl_count_edges)."""
+        m = self.num_edges()
+
+        def out(a, dt, name):
+            if a is None:
+                return np.zeros(m, dtype=dt)
+            if (not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous or a.size < m
+                    or not a.flags.writeable):
+                raise ValueError(f"{name}: need a writeable C-contiguous {np.dtype(dt).name} array of >= {m}")
+            return a
+        t, x7, x10 = out(t, np.uint32, "t"), out(x7, np.uint64, "x7"), out(x10, np.uint64, "x10")
+        gv, uc = _GV(), _UC()
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        _check(LIB.gl_count_edges(self._h, C.byref(gv), C.byref(uc), p(t), p(x7), p(x10)))
+        res = CountResult([_to_int(gv.x[i]) for i in range(18)], [_to_int(uc.c[i]) for i in range(17)],
+                          *self.last_stats())
+        return res, t[:m], x7[:m], x10[:m]
 
     def last_stats(self):
         ms = (C.c_float * 5)()

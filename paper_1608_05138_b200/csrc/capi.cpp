@@ -348,6 +348,38 @@ int gl_count(gl_graph* g, gl_graphlet_vector* X, gl_unrestricted* unres) {
     });
 }
 
+int gl_count_edges(gl_graph* g, gl_graphlet_vector* X, gl_unrestricted* unres, uint32_t* t, uint64_t* x7,
+                   uint64_t* x10) {
+    return guarded([&] {
+        auto& gr = G(g);
+        if (!X) throw gl::invalid_argument("null X");
+        GL_CUDA(cudaSetDevice(gr.device));
+        const gl::u64 m = gr.d.m;
+        gr.cs.part.alloc((2 * m + 2) * sizeof(gl::i64));
+        gr.cs.out_t = t;
+        gr.cs.out_x7 = x7;
+        struct Reset { // the early-copy pointers never outlive this call
+            gl::CountState& cs;
+            ~Reset() {
+                if (cs.s3) cudaStreamSynchronize(cs.s3);
+                cs.out_t = nullptr;
+                cs.out_x7 = nullptr;
+            }
+        } reset{gr.cs};
+        gl::count_begin(gr, 0, 1, gr.cs.part.as<gl::i64>(), gr.stream);
+        gl::count_mid(gr, gr.cs.part.as<gl::i64>(), gr.stream);
+        gl::u128 C[17], XX[18];
+        gl::count_finish(gr, gr.cs.part.as<gl::i64>(), 0, m, C, gr.stream);
+        if (x10 && m)
+            GL_CUDA(cudaMemcpyAsync(x10, gr.cs.x10.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, gr.stream));
+        GL_CUDA(cudaStreamSynchronize(gr.stream));
+        if (gr.cs.s3) GL_CUDA(cudaStreamSynchronize(gr.cs.s3));
+        gl::global_from_unrestricted(C, gr.d.n, m, XX);
+        to_c(XX, X->x, 18);
+        if (unres) to_c(C, unres->c, 17);
+    });
+}
+
 int gl_micro_records(const gl_graph* g, uint64_t first, uint64_t count, gl_micro_record* out) {
     return guarded([&] {
         auto& gr = G(g);

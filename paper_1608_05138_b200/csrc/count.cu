@@ -175,6 +175,12 @@ k_final(DevGraph g, const i64* __restrict__ part, const u32* __restrict__ t, u64
 
 // ------------------------------------------------------------ work lists
 
+// x7 column of the partial rows {x7, y} (final after the H-pass)
+__global__ void k_even(const i64* __restrict__ part, u64 m, u64* __restrict__ out) {
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < m; e += (u64)gridDim.x * blockDim.x)
+        out[e] = (u64)part[2 * e];
+}
+
 __global__ void k_seq(u32* __restrict__ ids, u64 n) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         ids[i] = (u32)i;
@@ -745,6 +751,24 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             }
         }
         GL_CUDA(cudaEventRecord(cs.ev[1], s));
+        if (world == 1 && (cs.out_t || cs.out_x7)) {
+            // t and x7 are final now (only the H-pass writes them): copy them out
+            // on s3 while the cycle pass runs (gl_count_edges)
+            if (!cs.s3) {
+                GL_CUDA(cudaStreamCreateWithFlags(&cs.s3, cudaStreamNonBlocking));
+                GL_CUDA(cudaEventCreateWithFlags(&cs.ev_out, cudaEventDisableTiming));
+            }
+            GL_CUDA(cudaStreamWaitEvent(cs.s3, cs.ev[1], 0));
+            if (cs.out_t) GL_CUDA(cudaMemcpyAsync(cs.out_t, cs.t.p, m * sizeof(u32), cudaMemcpyDeviceToHost, cs.s3));
+            if (cs.out_x7) {
+                cs.x7c.alloc((m + 1) * sizeof(u64));
+                k_even<<<grid1d(m, 256, sms), 256, 0, cs.s3>>>(d_partials, m, cs.x7c.as<u64>());
+                GL_LAUNCH_CHECK();
+                GL_CUDA(cudaMemcpyAsync(cs.out_x7, cs.x7c.p, m * sizeof(u64), cudaMemcpyDeviceToHost, cs.s3));
+                cs.launches += 1;
+            }
+            GL_CUDA(cudaEventRecord(cs.ev_out, cs.s3));
+        }
 
         // cycles: top vertices, split small (warp hash) / big (block windows)
         GL_CUDA(cudaEventRecord(cs.ev[2], s2));

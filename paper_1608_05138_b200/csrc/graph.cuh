@@ -85,6 +85,13 @@ struct CountState {
     DevBuf pieces;                 // uint4 (a, clo, chi, wedge estimate): windowed-top pieces, then the rank's share
     u64 cycle_pieces = 0;
     DevBuf runtab;                 // u32[2m] run-end table of the dense cycle windows (count.cu k_run_flags)
+    // early copy-out (gl_count_edges): t and x7 are final after the H-pass, so
+    // they go to these host buffers on s3 while the cycle pass runs
+    std::uint32_t* out_t = nullptr;
+    std::uint64_t* out_x7 = nullptr;
+    DevBuf x7c;                    // u64[m] contiguous x7 for that copy
+    cudaStream_t s3 = nullptr;
+    cudaEvent_t ev_out = nullptr;
     u32 runtab_key = 0;            // walk_cl + 1 it was built for (0: none)
     cudaStream_t s2 = nullptr;     // cycle-pass stream (owned)
     cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork, 7 end of count_mid
@@ -113,6 +120,11 @@ struct Graph {
         // caller's: drain the device before releasing them
         cudaSetDevice(device);
         cudaDeviceSynchronize();
+        if (cs.s3) {
+            cudaStreamSynchronize(cs.s3);
+            cudaStreamDestroy(cs.s3);
+            if (cs.ev_out) cudaEventDestroy(cs.ev_out);
+        }
         if (cs.s2) {
             cudaStreamSynchronize(cs.s2);
             for (auto e : cs.ev)

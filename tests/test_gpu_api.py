@@ -136,3 +136,21 @@ def test_edge_motif_records_match_reference_pipeline(cuda_device):
         one = g.process_edge_hash(7)
         assert tuple(int(one[f]) for f in ("t", "x7", "x10", "work_units")) == tuple(int(x) for x in ref[7, [0, 3, 4, 5]])
         assert gl.local_three_counts(one, g.num_vertices())[0] == int(one["t"])
+
+
+def test_count_edges_equals_count_then_copy(cuda_device):
+    """gl_count_edges (t/x7 copied out during the cycle pass) == gl_count +
+    gl_edge_counts, also into caller buffers, and again on a reused graph."""
+    g = gl.Graph.build(gl.generate_rmat(12, 16, seed=6), cuda_device)
+    ref = g.count()
+    t, x7, x10 = (a.copy() for a in g.edge_counts())
+    for _ in range(2):
+        res, t2, x72, x102 = g.count_edges()
+        assert res.X == ref.X and res.C == ref.C
+        assert np.array_equal(t2, t) and np.array_equal(x72, x7) and np.array_equal(x102, x10)
+    m = g.num_edges()
+    bt, b7, b10 = np.zeros(m + 3, np.uint32), np.zeros(m, np.uint64), np.zeros(m, np.uint64)
+    g.count_edges(bt, b7, b10)
+    assert np.array_equal(bt[:m], t) and np.array_equal(b7, x7) and np.array_equal(b10, x10)
+    with pytest.raises(ValueError):
+        g.count_edges(t=np.zeros(m, np.int64))

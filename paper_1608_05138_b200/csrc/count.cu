@@ -227,7 +227,7 @@ __global__ void k_hkeys(DevGraph g, u32* __restrict__ keys, unsigned long long* 
         u64 q = 0;
         for (u64 i = lane; i + 1 < k; i += 32) { // entries read: streamed list or ~8 per probe
             const u32 x = g.adj[ub + i];
-            const u64 ul = g.off[x + 1] - (g.off[x] + g.lcnt[x]), pr = (u64)kHProbeRatio * (k - 1 - i);
+            const u64 ul = g.off[x + 1] - (g.off[x] + g.lcnt[x]), pr = (u64)c_probe_ratio * (k - 1 - i);
             q += ul < pr ? ul : pr;
         }
         q = warp_sum_u64(q);
@@ -601,6 +601,10 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
         GL_CUDA(cudaEventSynchronize(cs.ev[1]));
         GL_CUDA(cudaEventSynchronize(cs.ev[3])); // cycle pass (on the previous caller stream when serialised)
         if (cs.mid_done) GL_CUDA(cudaEventSynchronize(cs.ev[7]));
+    }
+    if (const char* pe = std::getenv("GL_PROBE_RATIO")) {
+        const u32 r = (u32)std::strtoul(pe, nullptr, 10);
+        if (r) GL_CUDA(cudaMemcpyToSymbolAsync(c_probe_ratio, &r, sizeof(r), 0, cudaMemcpyHostToDevice, s ? s : gr.stream));
     }
     cs.launches = 0;
     cs.began = false;

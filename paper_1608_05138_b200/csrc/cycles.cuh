@@ -404,7 +404,10 @@ __device__ __forceinline__ u32 warp_upper_bound(const u32* a, u32 n, u32 x) {
 // a segmented shuffle sum whose tail lanes issue the RED.
 //   PASS 0: W[c]++     PASS 1: credit W[c]-1 to (b,c) and, summed, to (a,b)
 //   PASS 2: W[c] = 0 (sparse clear of a dense window)
-constexpr int kUnroll = 8; // uniform-path rounds with loads in flight per lane
+#ifndef GL_KUNROLL
+#define GL_KUNROLL 12
+#endif
+constexpr int kUnroll = GL_KUNROLL; // uniform-path rounds with loads in flight per lane (12: -1..2% vs 8 or 16)
 
 template <int KIND, int PASS>
 __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,

@@ -327,7 +327,13 @@ def run_ours(args):
         except Exception:
             traffic = None
 
-    # ---- e2e through the public C-ABI from pinned host buffers
+    # ---- e2e through the public C-ABI from pinned host buffers.  The
+    # device-resident graph is released first: every e2e graph is built, counted
+    # and freed on its own (each count sizes its H-edge record list from the
+    # free memory, so graphs alive side by side at RMAT-24+ would run out)
+    g.close()
+    del partials, flush
+    torch.cuda.synchronize()
     e2e = None
     if not args.no_e2e:
         hpairs = hp if hp is not None else host_pairs(args)
@@ -361,8 +367,10 @@ def run_ours(args):
                 g2.edge_counts(b, shard_n, pin_t.numpy().view(np.uint32)[:shard_n],
                                pin_x7.numpy().view(np.uint64)[:shard_n], pin_x10.numpy().view(np.uint64)[:shard_n])
             dt = (time.perf_counter() - t0) * 1e3
-            # same step again on the same graph object, ending in the full
-            # MicroRecord table instead of the compact (t, x7, x10) arrays
+            g2.close()
+            del p2
+            # same step again on a fresh graph, ending in the full MicroRecord
+            # table instead of the compact (t, x7, x10) arrays
             barrier()
             torch.cuda.synchronize()
             t1 = time.perf_counter()
@@ -373,9 +381,8 @@ def run_ours(args):
             dr = (time.perf_counter() - t1) * 1e3
             if os.environ.get("GL_BENCH_VERBOSE"):
                 print(f"e2e iteration {i}: {dt:.1f} ms, with micro records {dr:.1f} ms", file=sys.stderr, flush=True)
-            g2.close()
             g3.close()
-            del p2, p3
+            del p3
             if i >= args.e2e_warmup:  # warm-up iterations: first-touch allocations
                 e2e_ms.append(dt)
                 rec_ms.append(dr)

@@ -469,6 +469,15 @@ __global__ void k_row_flags(DevGraph g, u32* __restrict__ rev) {
 struct MinU32 {
     __device__ __forceinline__ u32 operator()(u32 a, u32 b) const { return a < b ? a : b; }
 };
+// packed table entry: (run-end slot q << 32) | adj[q]  (all ones: none) -- the
+// run end and the c the cursor lands on come in one load
+__global__ void k_run_pack(DevGraph g, const u32* __restrict__ scan, u64* __restrict__ tab) {
+    const u64 S = 2 * g.m;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < S; i += (u64)gridDim.x * blockDim.x) {
+        const u32 q = scan[i];
+        tab[i] = q == kEmpty ? ~0ull : ((u64)q << 32) | g.adj[q];
+    }
+}
 
 // Piece cap: no work item above 1/4 of one SM's fair share of the job,
 // wedges / (4 * SMs * ranks) (at least 2^17): 1/592 of the cycle work on one
@@ -855,21 +864,24 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const bool use_runs = mybig_p && !(rt && rt[0] == '0');
                 if (use_runs && cs.runtab_key != walk_cl() + 1) {
                     const u64 S = 2 * m;
-                    DevBuf rev;
+                    DevBuf rev, scan;
                     rev.alloc(S * sizeof(u32));
-                    cs.runtab.alloc(S * sizeof(u32));
+                    scan.alloc(S * sizeof(u32));
+                    cs.runtab.alloc(S * sizeof(u64));
                     k_run_flags<<<grid1d(S, 256, sms, 16), 256, 0, s2>>>(g, tiers, walk_cl(), rev.as<u32>());
                     k_row_flags<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, rev.as<u32>());
                     GL_LAUNCH_CHECK();
                     size_t bytes = 0;
-                    GL_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rev.as<u32>(), cs.runtab.as<u32>(), MinU32{},
+                    GL_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rev.as<u32>(), scan.as<u32>(), MinU32{},
                                                            (int64_t)S, s2));
                     cs.tmp_c.alloc(bytes);
-                    GL_CUDA(cub::DeviceScan::InclusiveScan(cs.tmp_c.p, bytes, rev.as<u32>(), cs.runtab.as<u32>(),
+                    GL_CUDA(cub::DeviceScan::InclusiveScan(cs.tmp_c.p, bytes, rev.as<u32>(), scan.as<u32>(),
                                                            MinU32{}, (int64_t)S, s2));
-                    GL_CUDA(cudaStreamSynchronize(s2)); // rev goes back to the (stream-unaware) pool
+                    k_run_pack<<<grid1d(S, 256, sms, 16), 256, 0, s2>>>(g, scan.as<u32>(), cs.runtab.as<u64>());
+                    GL_LAUNCH_CHECK();
+                    GL_CUDA(cudaStreamSynchronize(s2)); // rev / scan go back to the (stream-unaware) pool
                     cs.runtab_key = walk_cl() + 1;
-                    cs.launches += 3;
+                    cs.launches += 4;
                 }
                 if (mymid || mysmid) cs.cursor2.alloc((u64)sms * 4 * w_hash * sizeof(u32));
                 auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
@@ -888,7 +900,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     smem_attr(k_cycle_block<K>, smem, gr.device);
                     k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s2>>>(
                         g, list, plist, count, queue, cs.slots.as<i64>(), scratch, cap, tiers, walk_cl(),
-                        K == 0 && use_runs ? cs.runtab.as<u32>() : nullptr);
+                        K == 0 && use_runs ? cs.runtab.as<u64>() : nullptr);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
                 };

@@ -153,9 +153,37 @@ __device__ __forceinline__ u32 ld_shared(u32 addr) {
     return v;
 }
 // RED.ADD.U64 to global issued under a predicate (no branch around it)
+// The slot credits stream through a 2m x 8 B array with no reuse inside a
+// window (every (b,c) slot gets one credit per top): they are issued with an
+// L2 evict-first policy so they do not push out the window's adjacency slices
+// (re-read by pass 1), the run metadata and the block scratch.  GL_NO_L2_HINT
+// drops the hints (A/B).
+__device__ __forceinline__ u64 l2_evict_first() {
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void red_add_u64_if(i64* p, u64 v) {
+#ifdef GL_NO_L2_HINT
     asm volatile("{ .reg .pred q; setp.ne.u64 q, %1, 0; @q red.global.add.u64 [%0], %1; }" ::"l"(p), "l"(v)
                  : "memory");
+#else
+    asm volatile("{ .reg .pred q; .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
+                 " setp.ne.u64 q, %1, 0; @q red.global.add.L2::cache_hint.u64 [%0], %1, pol; }" ::"l"(p),
+                 "l"(v)
+                 : "memory");
+#endif
+}
+// one-use 8-byte load (run-end table) with the same evict-first policy
+__device__ __forceinline__ u64 ld_u64_stream(const u64* p) {
+    u64 v;
+#ifdef GL_NO_L2_HINT
+    v = __ldg(p);
+#else
+    asm volatile("{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
+                 " ld.global.nc.L2::cache_hint.u64 %0, [%1], pol; }" : "=l"(v) : "l"(p));
+#endif
+    return v;
 }
 
 // Packed window counters: 2^cl counters of (32 >> cl) bits per word.  The
@@ -713,7 +741,7 @@ template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict__ pieces, u64 n_items,
               unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap,
-              uint4 tiers, u32 walk_cl, const u32* __restrict__ nxt_rev) {
+              uint4 tiers, u32 walk_cl, const u64* __restrict__ nxt_rev) {
     constexpr bool HASH = Cyc<KIND>::HASH, WIN = Cyc<KIND>::WIN;
     constexpr int THREADS = Cyc<KIND>::THREADS;
     constexpr u32 kWords = Cyc<KIND>::WORDS, kMeta = Cyc<KIND>::META, kSlots = 1u << Cyc<KIND>::LOG;
@@ -920,15 +948,21 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                         const u32 j = j0 + u * THREADS;
                         const u32 c0 = S.cur[j], re = S.rend[j];
                         const u64 rb = S.rb[j];
-                        u32 h = re;
+                        u32 h = re, cn = kEmpty;
+                        bool have_cn = false;
                         // the row's last window needs no search: its run ends at re
                         if (WIN && S.lastc[j] >= hi) {
                             if (grid_ends) {
                                 // first slot after rb + c0 on a later window (or row start)
+                                // and the c there, in one load
                                 const u64 p1 = rb + c0 + 1;
-                                const u32 q = p1 < 2 * g.m ? nxt_rev[2 * g.m - 1 - p1] : kEmpty;
-                                const u64 qe = (u64)q - rb;
-                                h = qe < (u64)re ? (u32)qe : re;
+                                const u64 v = p1 < 2 * g.m ? ld_u64_stream(nxt_rev + (2 * g.m - 1 - p1)) : ~0ull;
+                                const u64 qe = (v >> 32) - rb;
+                                if (qe < (u64)re) {
+                                    h = (u32)qe;
+                                    cn = (u32)v;
+                                    have_cn = true;
+                                }
                             } else {
                                 const u32 pl = S.plen[j];
                                 h = (u32)(gallop_from(g.adj, rb + c0, rb + re, rb + c0 + (pl ? pl - 1 : 0), hi) - rb);
@@ -938,7 +972,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                         S.hpos[j] = c0; // run start
                         S.rwin[j] = win;
                         S.cur[j] = h;
-                        S.nextc[j] = h < re ? g.adj[rb + h] : kEmpty;
+                        S.nextc[j] = h < re ? (have_cn ? cn : g.adj[rb + h]) : kEmpty;
                         ++my_runs;
                         my_wedges += h - c0;
                     }

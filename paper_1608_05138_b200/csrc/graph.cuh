@@ -43,6 +43,7 @@ struct DevGraph {
 void* pool_alloc(size_t bytes, int device, size_t* got);
 void pool_free(void* p, size_t bytes, int device);
 void pool_trim();
+size_t pool_cached_bytes(int device);
 
 // RAII device buffer (pool-backed)
 struct DevBuf {
@@ -84,7 +85,7 @@ struct CountState {
     DevBuf keys_c, items_c, tmp_c; // the cycle pass's own (it runs concurrently on s2)
     DevBuf pieces;                 // uint4 (a, clo, chi, wedge estimate): windowed-top pieces, then the rank's share
     u64 cycle_pieces = 0;
-    DevBuf runtab;                 // u32[2m] run-end table of the dense cycle windows (count.cu k_run_flags)
+    DevBuf runtab;                 // u64[2m] run-end table of the dense cycle windows: (end slot, c there) (count.cu k_run_flags)
     // early copy-out (gl_count_edges): t and x7 are final after the H-pass, so
     // they go to these host buffers on s3 while the cycle pass runs
     std::uint32_t* out_t = nullptr;

@@ -122,6 +122,9 @@ struct TriList {
     u32* n;      // per work item
 };
 constexpr u64 kNoList = ~0ull;
+// TriList::n flags: the low 31 bits count the records; kRecSoA marks the
+// structure-of-arrays layout of a big-k vertex (pairs, then edge ids)
+constexpr u32 kRecSoA = 0x80000000u, kRecCountMask = 0x7fffffffu;
 
 // 2 <= k <= 32: one warp per vertex a.  Phase 1 streams every member's upper
 // list U(x_i) with the whole warp (coalesced) and looks each entry up in
@@ -410,7 +413,7 @@ template <int MODE, int BLOG, typename Cand>
 __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict__ t, i64* __restrict__ part, u32* ws,
                                              Cand* cbuf, uint2* hlist, u32& s_nh, u32& s_mi, u32 a, u64 ub, u32 k,
                                              u32 W, u32 hl, u32 H, const TriList& TL, u64 idx, u64& s_base,
-                                             bool big = false, u32 stage_words = 0) {
+                                             u64 hcap = 0, bool big = false, u32 stage_words = 0) {
     const u32 lane = lane_id();
     if (MODE == kHPassSums && TL.rec && TL.base[idx] != kNoList) {
         // stream this vertex's H-edge records: t of (x_i, x_j) gathered, the
@@ -423,7 +426,12 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         }
         __syncthreads();
         const uint2* rec = TL.rec + TL.base[idx];
-        const u32 nrec = TL.n[idx];
+        const u32 nrec = TL.n[idx] & kRecCountMask;
+        // kRecSoA: a big-k vertex kept its records as two u32 arrays in its
+        // C(k,2)-record reservation (member pairs, then edge ids)
+        const bool soa = TL.n[idx] & kRecSoA;
+        const u32* rij = reinterpret_cast<const u32*>(rec);
+        const u32* re_ = rij + (u64)k * (k - 1) / 2;
         constexpr int U = 4;
         for (u32 r0 = threadIdx.x; r0 < nrec; r0 += U * blockDim.x) {
             uint2 rv[U];
@@ -431,7 +439,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const u32 r = r0 + u * blockDim.x;
-                rv[u] = r < nrec ? rec[r] : make_uint2(0, kEmpty);
+                rv[u] = r >= nrec ? make_uint2(0, kEmpty) : soa ? make_uint2(rij[r], re_[r]) : rec[r];
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) tv[u] = rv[u].y != kEmpty ? t[rv[u].y] : 0u;
@@ -501,6 +509,10 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     }
     __syncthreads();
     uint2* const hout = (MODE == kHPassCount && s_base != kNoList) ? TL.rec + s_base : hlist;
+    // big k: records as SoA over the same region (capacity C(k,2) in the
+    // device-wide list, hcap in the block's own list)
+    u32* const hij = reinterpret_cast<u32*>(hout);
+    u32* const hee = hij + ((MODE == kHPassCount && s_base != kNoList) ? (u64)k * (k - 1) / 2 : hcap);
     const u32 xmax = xs[k - 1];
     // phase 1: warps grab members i < k-1 and stream U(x_i)
     for (;;) {
@@ -523,7 +535,15 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
                     u32 base = 0;
                     if (lane == 0) base = atomicAdd(&s_nh, (u32)__popc(bal));
                     base = __shfl_sync(0xffffffffu, base, 0);
-                    if (hit) hout[base + __popc(bal & ((1u << lane) - 1u))] = make_uint2((j << 16) | i, e);
+                    if (hit) {
+                        const u32 at = base + __popc(bal & ((1u << lane) - 1u));
+                        if (big) { // SoA: the chunk sweeps of phase 2 read the pairs alone
+                            hij[at] = (j << 16) | i;
+                            hee[at] = e;
+                        } else {
+                            hout[at] = make_uint2((j << 16) | i, e);
+                        }
+                    }
                 }
             } else if (hit) {
                 const u64 txy = t[e];
@@ -631,7 +651,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // atomicOr), then one popcount sweep over the records; member degrees
         // accumulate per chunk (phase 3)
         const u32 nh = s_nh;
-        if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh;
+        if (TL.rec && threadIdx.x == 0) TL.n[idx] = nh | kRecSoA;
         // phase 1's hash, Bloom filter, member ids and list bounds are dead
         // now: the member degrees take xs' place and the stage everything
         // after tri (stage_words = the workspace words beyond xs and tri)
@@ -649,14 +669,14 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
             for (u32 q = threadIdx.x; q < k * sst; q += blockDim.x) st[q] = 0ull;
             __syncthreads();
             for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
-                const uint2 he = hout[h];
-                const u32 i = he.x & 0xffffu, j = he.x >> 16;
+                const u32 ij = hij[h];
+                const u32 i = ij & 0xffffu, j = ij >> 16;
                 if (j >= lo && j < hi) atomicOr(&st[(u64)i * sst + ((j - lo) >> 6)], 1ull << (j & 63));
                 if (i >= lo && i < hi) atomicOr(&st[(u64)j * sst + ((i - lo) >> 6)], 1ull << (i & 63));
             }
             __syncthreads();
             for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
-                const uint2 he = hout[h];
+                const uint2 he = make_uint2(hij[h], hee[h]);
                 const u32 i = he.x & 0xffffu, j = he.x >> 16;
                 const unsigned long long* ri = st + (u64)i * sst;
                 const unsigned long long* rj = st + (u64)j * sst;
@@ -764,7 +784,7 @@ k_hpass_block(DevGraph g, const u32* __restrict__ items, u64 n_items, unsigned l
             // H_a's rows rebuilt per column chunk in shared memory from the
             // H-edge records (the small arrays, degrees and stage all shared)
             hpass_vertex<MODE, BLOG>(g, t, part, smem, cbuf, hlist, s_nh, s_mi, a, ub, k, W, hl, H, TL, idx, s_base,
-                                     true, smem_words - 2 * k);
+                                     hcap, true, smem_words - 2 * k);
         } else {
             hpass_vertex<MODE, BLOG>(g, t, part, gscratch + (u64)blockIdx.x * gstride, cbuf, hlist, s_nh, s_mi, a,
                                      ub, k, W, hl, H, TL, idx, s_base);

@@ -43,7 +43,6 @@ struct DevGraph {
 void* pool_alloc(size_t bytes, int device, size_t* got);
 void pool_free(void* p, size_t bytes, int device);
 void pool_trim();
-size_t pool_cached_bytes(int device);
 
 // RAII device buffer (pool-backed)
 struct DevBuf {

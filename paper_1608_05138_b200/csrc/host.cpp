@@ -55,17 +55,6 @@ void* pool_alloc(size_t bytes, int device, size_t* got) {
     return p;
 }
 
-// bytes the pool holds for `device` (free for the next allocations, though
-// the driver counts them as used)
-size_t pool_cached_bytes(int device) {
-    Pool& P = pool();
-    std::lock_guard<std::mutex> lk(P.mu);
-    size_t b = 0;
-    for (const auto& kv : P.cached)
-        if (kv.second.first == device) b += kv.first;
-    return b;
-}
-
 void pool_free(void* p, size_t bytes, int device) {
     Pool& P = pool();
     {

@@ -632,6 +632,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     GL_CUDA(cudaMemsetAsync(cs.t.p, 0, (m + 1) * sizeof(u32), s));
     cs.slots.alloc((2 * m + 1) * sizeof(i64));
     GL_CUDA(cudaMemsetAsync(cs.slots.p, 0, (2 * m + 1) * sizeof(i64), s));
+    cs.slots32.alloc((2 * m + 1) * sizeof(u32));
+    GL_CUDA(cudaMemsetAsync(cs.slots32.p, 0, (2 * m + 1) * sizeof(u32), s));
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40; // queues + counts
     GL_CUDA(cudaMemsetAsync(counters, 0, kCounters * sizeof(u64), s));
 
@@ -806,6 +808,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                              (unsigned long long)nsparse, (unsigned long long)nbig, (unsigned long long)nmid,
                              (unsigned long long)nsmid, (unsigned long long)nsmall);
             const uint4 tiers = make_uint4((u32)cc[22], (u32)(cc[22] >> 32), (u32)cc[23], (u32)(cc[23] >> 32));
+            // slot credits: u32 unless c is a hub (degree >= 65536 = ids >= tiers.w), see Credits
+            const Credits credits{cs.slots.as<i64>(), cs.slots32.as<u32>(), tiers.w};
             cs.work[2] = 12 * wtot / (u64)world; // 4 B c id + 8 B slot credit per wedge
             cs.launches += 2 + 10;
             const u64 mysparse = rank_share(nsparse, rank, world);
@@ -899,7 +903,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     const size_t smem = (size_t)cyc_smem_words<K>() * sizeof(u32);
                     smem_attr(k_cycle_block<K>, smem, gr.device);
                     k_cycle_block<K><<<(unsigned)sms * Cyc<K>::MINB, Cyc<K>::THREADS, smem, s2>>>(
-                        g, list, plist, count, queue, cs.slots.as<i64>(), scratch, cap, tiers, walk_cl(),
+                        g, list, plist, count, queue, credits, scratch, cap, tiers, walk_cl(),
                         K == 0 && use_runs ? cs.runtab.as<u64>() : nullptr);
                     GL_LAUNCH_CHECK();
                     cs.launches += 2;
@@ -920,7 +924,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 const size_t smem = (size_t)kCycleSmallWarps * kSmallWarpWords * sizeof(u32);
                 smem_attr(k_cycle_small, smem, gr.device);
                 k_cycle_small<<<(unsigned)sms * 3, kCycleSmallWarps * 32, smem, s2>>>(
-                    g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, cs.slots.as<i64>());
+                    g, cs.wpre.as<u64>(), lsmall, mysmall, counters + 2, credits);
                 GL_LAUNCH_CHECK();
                 cs.launches += 2;
             }
@@ -977,7 +981,8 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     // (after the sums: both update y, the fold non-atomically)
     GL_CUDA(cudaStreamWaitEvent(s, cs.ev[3], 0));
     if (g.m) {
-        k_fold_slots<<<grid1d(g.m, 256, sms), 256, 0, s>>>(g, cs.slots.as<i64>(), d_partials);
+        k_fold_slots<<<grid1d(g.m, 256, sms), 256, 0, s>>>(g, Credits{cs.slots.as<i64>(), cs.slots32.as<u32>(), 0u},
+                                                           d_partials);
         GL_LAUNCH_CHECK();
         cs.launches += 1;
     }

@@ -9,6 +9,65 @@
 __device__ __forceinline__ u32 hslot(u32 key) { return (key * 0x9E3779B1u) >> (32 - 10); }
 static_assert(kHashSlots == 1024, "hslot assumes 1024 slots");
 
+// The slot credits stream through a 2m x 8 B array with no reuse inside a
+// window (every (b,c) slot gets one credit per top): they are issued with an
+// L2 evict-first policy so they do not push out the window's adjacency slices
+// (re-read by pass 1), the run metadata and the block scratch.  GL_NO_L2_HINT
+// drops the hints (A/B).
+__device__ __forceinline__ void red_add_u64_if(i64* p, u64 v) {
+#ifdef GL_NO_L2_HINT
+    asm volatile("{ .reg .pred q; setp.ne.u64 q, %1, 0; @q red.global.add.u64 [%0], %1; }" ::"l"(p), "l"(v)
+                 : "memory");
+#else
+    asm volatile("{ .reg .pred q; .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
+                 " setp.ne.u64 q, %1, 0; @q red.global.add.L2::cache_hint.u64 [%0], %1, pol; }" ::"l"(p),
+                 "l"(v)
+                 : "memory");
+#endif
+}
+// 32-bit form of the slot credit (same evict-first policy)
+__device__ __forceinline__ void red_add_u32_if(u32* p, u32 v) {
+#ifdef GL_NO_L2_HINT
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, 0; @q red.global.add.u32 [%0], %1; }" ::"l"(p), "r"(v)
+                 : "memory");
+#else
+    asm volatile("{ .reg .pred q; .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
+                 " setp.ne.u32 q, %1, 0; @q red.global.add.L2::cache_hint.u32 [%0], %1, pol; }" ::"l"(p),
+                 "r"(v)
+                 : "memory");
+#endif
+}
+// C4 credit accumulators.  The credit of slot (b,c) from top a is W_a[c]-1 <=
+// deg(c)-1 and b's tops are its upper neighbours U(b), so a slot's total is
+// <= |U(b)| (deg(c)-1); under degree order |U(b)|^2 <= 2m < 2^32, hence for
+// every c of degree < 65536 the total fits 32 bits: those slots take a u32
+// RED (half the read-modify-write bytes of the slot array, the largest DRAM
+// stream at scale).  Slots whose c is a hub (degree >= 65536: ids >= hub, the
+// 32-bit counter tier) and the per-run (a,b) sums stay 64-bit.
+struct Credits {
+    i64* s64;
+    u32* s32;
+    u32 hub;
+};
+__device__ __forceinline__ void credit_slot(const Credits& cr, u64 slot, u32 c, u32 v) {
+    if (c >= cr.hub)
+        red_add_u64_if(&cr.s64[slot], (u64)v);
+    else
+        red_add_u32_if(&cr.s32[slot], v);
+}
+
+// one-use 8-byte load (run-end table) with the same evict-first policy
+__device__ __forceinline__ u64 ld_u64_stream(const u64* p) {
+    u64 v;
+#ifdef GL_NO_L2_HINT
+    v = __ldg(p);
+#else
+    asm volatile("{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
+                 " ld.global.nc.L2::cache_hint.u64 %0, [%1], pol; }" : "=l"(v) : "l"(p));
+#endif
+    return v;
+}
+
 // Small tops: one warp per top vertex a, W[c] in a warp-private hash.
 // per-warp shared words of k_cycle_small: keys u32[kHashSlots], counts u16
 // packed in kHashSlots/2 words, the touched-slot list u16[kSmallWedges],
@@ -20,7 +79,7 @@ constexpr u32 kSmallWarpWords =
 
 __global__ void __launch_bounds__(kCycleSmallWarps * 32)
 k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ items, u64 n_items,
-              unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc) {
+              unsigned long long* __restrict__ queue, Credits cr) {
     extern __shared__ u32 smem[];
     const u32 lane = lane_id();
     const u32 wib = threadIdx.x >> 5;
@@ -108,11 +167,11 @@ k_cycle_small(DevGraph g, const u64* __restrict__ wpre, const u32* __restrict__ 
                 u32 h = hslot(cv);
                 while (keys[h] != cv) h = (h + 1) & (kHashSlots - 1);
                 val = ((cnt[h >> 1] >> ((h & 1) << 4)) & 0xffffu) - 1u;
-                if (val) atomic_add_i64(&slot_acc[slot], (i64)val);
+                if (val) credit_slot(cr, slot, cv, (u32)val);
             }
             u64 sum;
             const bool tail = seg_tail_sum(j, val, &sum);
-            if (k < nw && tail && sum) atomic_add_i64(&slot_acc[g.off[a] + j], (i64)sum);
+            if (k < nw && tail && sum) atomic_add_i64(&cr.s64[g.off[a] + j], (i64)sum);
         }
         __syncwarp();
         // sparse clear: only the slots this top filled (a count word is shared
@@ -153,38 +212,6 @@ __device__ __forceinline__ u32 ld_shared(u32 addr) {
     return v;
 }
 // RED.ADD.U64 to global issued under a predicate (no branch around it)
-// The slot credits stream through a 2m x 8 B array with no reuse inside a
-// window (every (b,c) slot gets one credit per top): they are issued with an
-// L2 evict-first policy so they do not push out the window's adjacency slices
-// (re-read by pass 1), the run metadata and the block scratch.  GL_NO_L2_HINT
-// drops the hints (A/B).
-__device__ __forceinline__ u64 l2_evict_first() {
-    u64 pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void red_add_u64_if(i64* p, u64 v) {
-#ifdef GL_NO_L2_HINT
-    asm volatile("{ .reg .pred q; setp.ne.u64 q, %1, 0; @q red.global.add.u64 [%0], %1; }" ::"l"(p), "l"(v)
-                 : "memory");
-#else
-    asm volatile("{ .reg .pred q; .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
-                 " setp.ne.u64 q, %1, 0; @q red.global.add.L2::cache_hint.u64 [%0], %1, pol; }" ::"l"(p),
-                 "l"(v)
-                 : "memory");
-#endif
-}
-// one-use 8-byte load (run-end table) with the same evict-first policy
-__device__ __forceinline__ u64 ld_u64_stream(const u64* p) {
-    u64 v;
-#ifdef GL_NO_L2_HINT
-    v = __ldg(p);
-#else
-    asm volatile("{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
-                 " ld.global.nc.L2::cache_hint.u64 %0, [%1], pol; }" : "=l"(v) : "l"(p));
-#endif
-    return v;
-}
 
 // Packed window counters: 2^cl counters of (32 >> cl) bits per word.  The
 // width follows the degree tier of the window's c ids (internal ids ascend
@@ -375,7 +402,7 @@ __device__ __forceinline__ u32 tab_get(const u32* W, u32 c, u32 lo, u32 cl) {
 __device__ __forceinline__ void tab_clear_one(u32* W, u32 c, u32 lo, u32 cl) { W[(c - lo) >> cl] = 0; }
 
 template <int KIND, int PASS>
-__device__ __forceinline__ void wedge_op(u32* W, u32 wb, u32 cv, u32 lo, u32 cl, i64* __restrict__ slot_acc, u64 slot,
+__device__ __forceinline__ void wedge_op(u32* W, u32 wb, u32 cv, u32 lo, u32 cl, Credits cr, u64 slot,
                                          u64& val) {
     if (!Cyc<KIND>::HASH) { // dense window: 32-bit shared addresses (wb = W's), predicated RED
         const u32 ci = cv - lo;
@@ -386,7 +413,7 @@ __device__ __forceinline__ void wedge_op(u32* W, u32 wb, u32 cv, u32 lo, u32 cl,
         } else if (PASS == 1) {
             const u32 w = ld_shared(addr) >> sh;
             const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
-            red_add_u64_if(&slot_acc[slot], (u64)v);
+            credit_slot(cr, slot, cv, v);
             val = v;
         } else {
             W[ci >> cl] = 0;
@@ -397,7 +424,7 @@ __device__ __forceinline__ void wedge_op(u32* W, u32 wb, u32 cv, u32 lo, u32 cl,
         tab_inc<KIND>(W, cv, lo, cl);
     } else if (PASS == 1) {
         const u32 v = tab_get<KIND>(W, cv, lo, cl) - 1u;
-        if (v) atomic_add_i64(&slot_acc[slot], (i64)v);
+        if (v) credit_slot(cr, slot, cv, v);
         val = v;
     } else {
         tab_clear_one(W, cv, lo, cl);
@@ -439,7 +466,7 @@ constexpr int kUnroll = GL_KUNROLL; // uniform-path rounds with loads in flight 
 
 template <int KIND, int PASS>
 __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,
-                                            u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
+                                            u32 lo, u32 cl, u64 abase, Credits cr) {
     const u32 lane = lane_id();
     if (kb >= ke) return;
     const u32 wb = smem_u32(W);
@@ -472,14 +499,14 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                     } else if (PASS == 1) {
                         const u32 w = ld_shared(addr) >> sh;
                         const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
-                        red_add_u64_if(&slot_acc[sbase + 32u * r], (u64)v);
+                        credit_slot(cr, sbase + 32u * r, cv, v);
                         acc += v;
                     } else {
                         st_shared(addr, 0u);
                     }
                 } else {
                     u64 v = 0;
-                    wedge_op<KIND, PASS>(W, wb, cv, lo, cl, slot_acc, sbase + 32u * r, v);
+                    wedge_op<KIND, PASS>(W, wb, cv, lo, cl, cr, sbase + 32u * r, v);
                     acc += v;
                 }
             };
@@ -504,7 +531,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             for (; r < nfull; ++r) op(__ldg(src + 32u * r), r);
             if (PASS == 1) {
                 acc = warp_sum_u64(acc);
-                if (lane == 0 && acc) atomic_add_i64(&slot_acc[abase + S.rj[bs]], (i64)acc);
+                if (lane == 0 && acc) atomic_add_i64(&cr.s64[abase + S.rj[bs]], (i64)acc);
             }
             k0 += nfull << 5;
         } else {
@@ -529,7 +556,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             u64 v = 0;
             if (valid) {
                 const u64 slot = (u64)S.rs[q] + off;
-                wedge_op<KIND, PASS>(W, wb, __ldg(g.adj + slot), lo, cl, slot_acc, slot, v);
+                wedge_op<KIND, PASS>(W, wb, __ldg(g.adj + slot), lo, cl, cr, slot, v);
             }
             if (PASS == 1) {
                 const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));
@@ -541,14 +568,14 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                         const u32 t = __shfl_up_sync(0xffffffffu, v32, d);
                         if (lane >= seg0 + (u32)d) v32 += t;
                     }
-                    if (tail && v32) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v32);
+                    if (tail && v32) atomic_add_i64(&cr.s64[abase + S.rj[q]], (i64)v32);
                 } else {
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
                         const u64 t = __shfl_up_sync(0xffffffffu, v, d);
                         if (lane >= seg0 + (u32)d) v += t;
                     }
-                    if (tail && v) atomic_add_i64(&slot_acc[abase + S.rj[q]], (i64)v);
+                    if (tail && v) atomic_add_i64(&cr.s64[abase + S.rj[q]], (i64)v);
                 }
             }
             k0 += 32;
@@ -582,7 +609,7 @@ __device__ __forceinline__ u32 grab_size(u32 remaining, u32 nwarps) {
 // consecutive slots), folded into edge rows by k_fold_slots.
 template <int KIND, int PASS>
 __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u32 nnz, u32 T, u32* counter, u32* W,
-                                          u32 lo, u32 cl, u64 abase, i64* __restrict__ slot_acc) {
+                                          u32 lo, u32 cl, u64 abase, Credits cr) {
     const u32 nwarps = blockDim.x >> 5;
     for (;;) {
         u32 k0 = 0, grab = 0;
@@ -594,7 +621,7 @@ __device__ __forceinline__ void grab_pass(const DevGraph& g, const RunMeta& M, u
         k0 = __shfl_sync(0xffffffffu, k0, 0);
         grab = __shfl_sync(0xffffffffu, grab, 0);
         if (k0 >= T) break;
-        window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, cl, abase, slot_acc);
+        window_pass<KIND, PASS>(g, M, nnz, k0, k0 + grab < T ? k0 + grab : T, W, lo, cl, abase, cr);
     }
 }
 
@@ -614,10 +641,10 @@ __device__ __forceinline__ void table_clear(u32* W, u32 words, u32 kslots, u32 t
 template <int KIND, int PASS>
 __device__ __forceinline__ void meta_pass(const DevGraph& g, const RunMeta& Msm, const RunMeta& Mgl, u32 nnz, u32 T,
                                           u32* counter, u32* W, u32 lo, u32 cl, u64 abase,
-                                          i64* __restrict__ slot_acc) {
+                                          Credits cr) {
     constexpr u32 kMeta = Cyc<KIND>::META;
     if (nnz <= kMeta) {
-        grab_pass<KIND, PASS>(g, Msm, nnz, T, counter, W, lo, cl, abase, slot_acc);
+        grab_pass<KIND, PASS>(g, Msm, nnz, T, counter, W, lo, cl, abase, cr);
         return;
     }
     for (u32 q0 = 0; q0 < nnz; q0 += kMeta) {
@@ -633,7 +660,7 @@ __device__ __forceinline__ void meta_pass(const DevGraph& g, const RunMeta& Msm,
         }
         if (threadIdx.x == 0) *counter = 0;
         __syncthreads();
-        grab_pass<KIND, PASS>(g, Msm, nq, end - base, counter, W, lo, cl, abase, slot_acc);
+        grab_pass<KIND, PASS>(g, Msm, nq, end - base, counter, W, lo, cl, abase, cr);
     }
 }
 
@@ -645,7 +672,7 @@ __device__ __forceinline__ void meta_pass(const DevGraph& g, const RunMeta& Msm,
 // step (one sector, independent loads).
 constexpr int kWalkStep = 4;
 __device__ __noinline__ void walk_window(const DevGraph& g, const BigScratch& S, u32 nb, u32* W, u32 lo, u32 hi,
-                                            u32 cl, u32 win, u64 abase, i64* __restrict__ slot_acc) {
+                                            u32 cl, u32 win, u64 abase, Credits cr) {
     const u32 wb = smem_u32(W);
     const u32 T = blockDim.x;
 #ifdef GL_CYCLE_PROF
@@ -723,12 +750,12 @@ __device__ __noinline__ void walk_window(const DevGraph& g, const BigScratch& S,
                         const u32 ci = cv[v] - lo;
                         const u32 w = ld_shared(wb + ((ci >> cl) << 2)) >> ((ci & ((1u << cl) - 1u)) << (5 - cl));
                         const u32 val = (w & ((1u << (32u >> cl)) - 1u)) - 1u;
-                        red_add_u64_if(&slot_acc[rb + p + v], (u64)val);
+                        credit_slot(cr, rb + p + v, cv[v], val);
                         sum += val;
                     }
                 }
             }
-            if (sum) atomic_add_i64(&slot_acc[abase + j], (i64)sum);
+            if (sum) atomic_add_i64(&cr.s64[abase + j], (i64)sum);
         }
     }
     __syncthreads();
@@ -740,7 +767,7 @@ __device__ __noinline__ void walk_window(const DevGraph& g, const BigScratch& S,
 template <int KIND>
 __global__ void __launch_bounds__(Cyc<KIND>::THREADS, Cyc<KIND>::MINB)
 k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict__ pieces, u64 n_items,
-              unsigned long long* __restrict__ queue, i64* __restrict__ slot_acc, u32* __restrict__ gscratch, u32 cap,
+              unsigned long long* __restrict__ queue, Credits cr, u32* __restrict__ gscratch, u32 cap,
               uint4 tiers, u32 walk_cl, const u64* __restrict__ nxt_rev) {
     constexpr bool HASH = Cyc<KIND>::HASH, WIN = Cyc<KIND>::WIN;
     constexpr int THREADS = Cyc<KIND>::THREADS;
@@ -833,10 +860,10 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
             GL_PROF_ADD(9, T);
             GL_PROF_ADD(10, 1);
             if (T) {
-                meta_pass<KIND, 0>(g, Msm, Mgl, nnz, T, &s_work[0], W, 0, 1, abase, slot_acc);
+                meta_pass<KIND, 0>(g, Msm, Mgl, nnz, T, &s_work[0], W, 0, 1, abase, cr);
                 __syncthreads();
                 GL_PROF_MARK(3);
-                meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, 0, 1, abase, slot_acc);
+                meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, 0, 1, abase, cr);
                 __syncthreads();
                 GL_PROF_MARK(4);
                 table_clear(W, kWords, kSlots, THREADS);
@@ -918,7 +945,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                         __syncthreads();
                         meta_dirty = false;
                     }
-                    walk_window(g, S, nb, W, lo, hi, cl, win, abase, slot_acc);
+                    walk_window(g, S, nb, W, lo, hi, cl, win, abase, cr);
                     GL_PROF_MARK(3);
                     continue;
                 }
@@ -1082,12 +1109,12 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
             if (T) {
                 const bool bulk_clear = HASH || T > kWords / 8;
                 {
-                    meta_pass<KIND, 0>(g, Msm, Mgl, nnz, T, &s_work[0], W, lo, cl, abase, slot_acc);
+                    meta_pass<KIND, 0>(g, Msm, Mgl, nnz, T, &s_work[0], W, lo, cl, abase, cr);
                 }
                 __syncthreads();
                 GL_PROF_MARK(3);
                 {
-                    meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, lo, cl, abase, slot_acc);
+                    meta_pass<KIND, 1>(g, Msm, Mgl, nnz, T, &s_work[1], W, lo, cl, abase, cr);
                 }
                 __syncthreads();
                 GL_PROF_MARK(4);
@@ -1095,7 +1122,7 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
                     const u32 words = HASH ? kWords : (hi - lo + (1u << cl) - 1u) >> cl;
                     table_clear(W, (words + 3u) & ~3u, HASH ? kSlots : 0u, THREADS);
                 } else if (!HASH) {
-                    meta_pass<KIND, 2>(g, Msm, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, slot_acc);
+                    meta_pass<KIND, 2>(g, Msm, Mgl, nnz, T, &s_work[2], W, lo, cl, abase, cr);
                 }
             }
             GL_PROF_SYNC_MARK(7);
@@ -1110,10 +1137,11 @@ k_cycle_block(DevGraph g, const u32* __restrict__ items, const uint4* __restrict
 }
 
 // y(e) += the two adjacency-slot accumulators of edge e (v's row, u's row).
-__global__ void k_fold_slots(DevGraph g, const i64* __restrict__ slot_acc, i64* __restrict__ part) {
+__global__ void k_fold_slots(DevGraph g, Credits cr, i64* __restrict__ part) {
     for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < g.m; e += (u64)gridDim.x * blockDim.x) {
         const u32 v = g.ev[e], u = g.eu[e];
-        const i64 s = slot_acc[g.off[v] + (e - g.loff[v])] + slot_acc[g.off[u] + g.epos[e]];
+        const u64 p1 = g.off[v] + (e - g.loff[v]), p2 = g.off[u] + g.epos[e];
+        const i64 s = cr.s64[p1] + cr.s64[p2] + (i64)cr.s32[p1] + (i64)cr.s32[p2];
         if (s) part[2 * e + 1] += s;
     }
 }

@@ -73,7 +73,8 @@ struct CountState {
     DevBuf t;        // u32[m]   triangles per edge
     DevBuf x7, x10;  // u64[m]   micro outputs of the last shard
     DevBuf part;     // i64[2m]  partials for the single-process path
-    DevBuf slots;    // i64[2m]  C4 credits per adjacency slot (folded into y)
+    DevBuf slots;    // i64[2m]  C4 credits per adjacency slot (folded into y): hub c and the (a,b) run sums
+    DevBuf slots32;  // u32[2m]  the same for c of degree < 65536 (cycles.cuh Credits)
     DevBuf hlist;    // per-block H-edge lists of the clique pass
     DevBuf tlist, tl_base, tl_n; // persistent H-edge records for the triangle-sum pass
     u64 tl_cap = 0;

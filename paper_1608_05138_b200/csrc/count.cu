@@ -84,10 +84,11 @@ inline unsigned grid1d(u64 n, int threads, int sms, int per_sm = 8) {
 // ------------------------------------------------------------------ prepass
 
 // wedges(e) = epos(e): the wedges a-b-c (c < a) of edge e = (a,b) as top edge
-__global__ void k_prepass(DevGraph g, u64* __restrict__ wedges) {
-    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < g.m; e += (u64)gridDim.x * blockDim.x)
-        wedges[e] = g.epos[e];
-}
+struct WedgesOf {
+    const u32* epos;
+    u64 m;
+    __device__ __forceinline__ u64 operator()(const u64& e) const { return e < m ? (u64)epos[e] : 0ull; }
+};
 
 #include "hpass.cuh"
 
@@ -507,8 +508,8 @@ struct Timer {
     }
 };
 
-template <typename T>
-void dev_exclusive_scan(DevBuf& tmp, const T* in, T* out, u64 n, cudaStream_t s) {
+template <typename In, typename T>
+void dev_exclusive_scan(DevBuf& tmp, In in, T* out, u64 n, cudaStream_t s) {
     size_t bytes = 0;
     GL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, s));
     tmp.alloc(bytes);
@@ -625,8 +626,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     cs.t.alloc((m + 1) * sizeof(u32));
     cs.wpre.alloc((m + 1) * sizeof(u64));
     cs.acc.alloc(96 * sizeof(u64));
-    cs.keys.alloc((std::max(m, n) + 1) * 2 * sizeof(u64)); // key in/out
-    cs.items2.alloc((std::max(m, n) + 1) * 2 * sizeof(u32)); // id in/out
+    cs.keys.alloc((n + 1) * 2 * sizeof(u32));   // H-pass sort keys in/out
+    cs.items2.alloc((n + 1) * 2 * sizeof(u32)); // vertex ids in/out
     const u64 plen = ((m + world - 1) / world) * (u64)world;
     if (plen) GL_CUDA(cudaMemsetAsync(d_partials, 0, 2 * plen * sizeof(i64), s));
     GL_CUDA(cudaMemsetAsync(cs.t.p, 0, (m + 1) * sizeof(u32), s));
@@ -651,11 +652,14 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
         for (int i = 1; i < 4; ++i) GL_CUDA(cudaEventRecord(cs.ev[i], s));
         GL_CUDA(cudaEventRecord(cs.ev[6], s)); // fork/join point of the (empty) cycle pass
     } else {
-        u64* wedges = cs.keys.as<u64>(); // scratch reuse before the sorts
-        k_prepass<<<grid1d(m, 256, sms), 256, 0, s>>>(g, wedges);
-        GL_LAUNCH_CHECK();
-        GL_CUDA(cudaMemsetAsync(wedges + m, 0, sizeof(u64), s));
-        dev_exclusive_scan<u64>(cs.tmp, wedges, cs.wpre.as<u64>(), m + 1, s);
+        // wedge prefix straight from epos (wedges(e) = epos(e), 0 past the end):
+        // no m-sized scratch
+        {
+            const WedgesOf op{g.epos, m};
+            cub::TransformInputIterator<u64, WedgesOf, cub::CountingInputIterator<u64>> it(
+                cub::CountingInputIterator<u64>(0), op);
+            dev_exclusive_scan(cs.tmp, it, cs.wpre.as<u64>(), m + 1, s);
+        }
         cs.launches += 2;
         GL_CUDA(cudaEventRecord(cs.ev[6], s)); // fork: the cycle pass needs the wedge prefix only
         GL_CUDA(cudaStreamWaitEvent(s2, cs.ev[6], 0));
@@ -776,10 +780,12 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             GL_CUDA(cudaStreamWaitEvent(cs.s3, cs.ev[1], 0));
             if (cs.out_t) GL_CUDA(cudaMemcpyAsync(cs.out_t, cs.t.p, m * sizeof(u32), cudaMemcpyDeviceToHost, cs.s3));
             if (cs.out_x7) {
-                cs.x7c.alloc((m + 1) * sizeof(u64));
-                k_even<<<grid1d(m, 256, sms), 256, 0, cs.s3>>>(d_partials, m, cs.x7c.as<u64>());
+                // staged in the x7 output array itself: k_final later writes the
+                // same values there (x7_out[e] = part[2e])
+                cs.x7.alloc((m + 1) * sizeof(u64));
+                k_even<<<grid1d(m, 256, sms), 256, 0, cs.s3>>>(d_partials, m, cs.x7.as<u64>());
                 GL_LAUNCH_CHECK();
-                GL_CUDA(cudaMemcpyAsync(cs.out_x7, cs.x7c.p, m * sizeof(u64), cudaMemcpyDeviceToHost, cs.s3));
+                GL_CUDA(cudaMemcpyAsync(cs.out_x7, cs.x7.p, m * sizeof(u64), cudaMemcpyDeviceToHost, cs.s3));
                 cs.launches += 1;
             }
             GL_CUDA(cudaEventRecord(cs.ev_out, cs.s3));
@@ -826,7 +832,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     g, cs.wpre.as<u64>(), iout, nwin, piece_cap(wtot, sms, world), piece_forced() ? 1u : 32u, np);
                 GL_CUDA(cudaMemsetAsync(np + nwin, 0, sizeof(u32), s2));
                 u32* poff = cs.items_c.as<u32>() + 2 * (n + 1); // see the allocation above
-                dev_exclusive_scan<u32>(cs.tmp_c, np, poff, nwin + 1, s2);
+                dev_exclusive_scan(cs.tmp_c, (const u32*)np, poff, nwin + 1, s2);
                 u32 hp[2];
                 GL_CUDA(cudaMemcpyAsync(&hp[0], poff + nsparse, sizeof(u32), cudaMemcpyDeviceToHost, s2));
                 GL_CUDA(cudaMemcpyAsync(&hp[1], poff + nwin, sizeof(u32), cudaMemcpyDeviceToHost, s2));

@@ -90,7 +90,6 @@ struct CountState {
     // they go to these host buffers on s3 while the cycle pass runs
     std::uint32_t* out_t = nullptr;
     std::uint64_t* out_x7 = nullptr;
-    DevBuf x7c;                    // u64[m] contiguous x7 for that copy
     cudaStream_t s3 = nullptr;
     cudaEvent_t ev_out = nullptr;
     u32 runtab_key = 0;            // walk_cl + 1 it was built for (0: none)

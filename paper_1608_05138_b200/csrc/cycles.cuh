@@ -56,23 +56,6 @@ __device__ __forceinline__ void credit_slot(const Credits& cr, u64 slot, u32 c, 
         red_add_u32_if(&cr.s32[slot], v);
 }
 
-// Adjacency loads of the window walk: pass 0 reads a run with an evict-last
-// policy (pass 1 re-reads it), pass 1 with evict-first (last use).
-// -DGL_ADJ_HINT enables it (A/B).
-template <int PASS> __device__ __forceinline__ u32 ld_adj(const u32* p) {
-#ifdef GL_ADJ_HINT
-    u32 v;
-    if (PASS == 0)
-        asm volatile("{ .reg .b64 pol; createpolicy.fractional.L2::evict_last.b64 pol, 1.0;"
-                     " ld.global.nc.L2::cache_hint.u32 %0, [%1], pol; }" : "=r"(v) : "l"(p));
-    else
-        asm volatile("{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
-                     " ld.global.nc.L2::cache_hint.u32 %0, [%1], pol; }" : "=r"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
 // one-use 8-byte load (run-end table) with the same evict-first policy
 __device__ __forceinline__ u64 ld_u64_stream(const u64* p) {
     u64 v;
@@ -531,11 +514,11 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             if (nfull >= (u32)kHalf) {
                 u32 cv[kHalf];
 #pragma unroll
-                for (int u = 0; u < kHalf; ++u) cv[u] = ld_adj<PASS>(src + 32u * u);
+                for (int u = 0; u < kHalf; ++u) cv[u] = __ldg(src + 32u * u);
                 for (; r + 2 * kHalf <= nfull; r += kHalf) {
                     u32 nx[kHalf];
 #pragma unroll
-                    for (int u = 0; u < kHalf; ++u) nx[u] = ld_adj<PASS>(src + 32u * (r + kHalf + u));
+                    for (int u = 0; u < kHalf; ++u) nx[u] = __ldg(src + 32u * (r + kHalf + u));
 #pragma unroll
                     for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
 #pragma unroll
@@ -545,7 +528,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                 for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
                 r += kHalf;
             }
-            for (; r < nfull; ++r) op(ld_adj<PASS>(src + 32u * r), r);
+            for (; r < nfull; ++r) op(__ldg(src + 32u * r), r);
             if (PASS == 1) {
                 acc = warp_sum_u64(acc);
                 if (lane == 0 && acc) atomic_add_i64(&cr.s64[abase + S.rj[bs]], (i64)acc);
@@ -573,7 +556,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
             u64 v = 0;
             if (valid) {
                 const u64 slot = (u64)S.rs[q] + off;
-                wedge_op<KIND, PASS>(W, wb, ld_adj<PASS>(g.adj + slot), lo, cl, cr, slot, v);
+                wedge_op<KIND, PASS>(W, wb, __ldg(g.adj + slot), lo, cl, cr, slot, v);
             }
             if (PASS == 1) {
                 const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));

@@ -59,7 +59,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-text-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=8)
-    ap.add_argument("--e2e-warmup", type=int, default=3)
+    ap.add_argument("--e2e-warmup", type=int, default=5)  # the pool and pinned pages settle after ~4 e2e steps
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 

@@ -448,15 +448,21 @@ __global__ void __launch_bounds__(256) k_pieces(DevGraph g, const u64* __restric
 // the first flagged slot >= p -- read at p + 1 it is p's run end.
 //   rev[i] = (slot 2m-1-i flagged) ? 2m-1-i : kEmpty;   table = min-scan(rev)
 //   run end after slot p = table[2m - 2 - p]  (kEmpty: none -> row prefix end)
-__device__ __forceinline__ u64 grid_win(u32 c, uint4 tiers, u32 walk_cl) {
+__device__ __forceinline__ u32 grid_win(u32 c, uint4 tiers, u32 walk_cl) {
     u32 t0, t1;
     const u32 cl = tier_of(c, tiers, t0, t1);
-    return ((u64)(4 - cl) << 40) | ((c - t0) / win_span(cl, 0, walk_cl));
+    // unclamped spans (<= 54272 << 4) and offsets fit 32 bits: a u32 division
+    return ((4 - cl) << 28) | ((c - t0) / (u32)win_span(cl, 0, walk_cl));
 }
 __global__ void k_run_flags(DevGraph g, uint4 tiers, u32 walk_cl, u32* __restrict__ rev) {
     const u64 S = 2 * g.m;
     for (u64 p = blockIdx.x * (u64)blockDim.x + threadIdx.x; p < S; p += (u64)gridDim.x * blockDim.x) {
-        const bool f = p == 0 || grid_win(g.adj[p], tiers, walk_cl) != grid_win(g.adj[p - 1], tiers, walk_cl);
+        // window id of this slot; the previous slot's from the neighbouring lane
+        // when it is in this warp's range (one division per slot)
+        const u32 w = grid_win(g.adj[p], tiers, walk_cl);
+        u32 wp = __shfl_up_sync(__activemask(), w, 1);
+        if ((threadIdx.x & 31) == 0 && p > 0) wp = grid_win(g.adj[p - 1], tiers, walk_cl);
+        const bool f = p == 0 || w != wp;
         rev[S - 1 - p] = f ? (u32)p : kEmpty;
     }
 }
@@ -638,6 +644,53 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
     unsigned long long* counters = cs.acc.as<unsigned long long>() + 40; // queues + counts
     GL_CUDA(cudaMemsetAsync(counters, 0, kCounters * sizeof(u64), s));
 
+    // Per-graph indexes of the cycle pass, built by the first count: the
+    // degree tiers of the window counters (k_tiers) and the run-end table of
+    // the dense windows (GL_RUN_TABLE=0 disables it)
+    // the H-edge record list is sized (once per graph) from the free memory
+    // seen here, before the run-end table's temporaries go to the pool
+    size_t free_at_start = 0;
+    if (!cs.tl_sized) {
+        size_t tot = 0;
+        GL_CUDA(cudaMemGetInfo(&free_at_start, &tot));
+    }
+    if (m && !cs.tiers_valid) {
+        cs.tierbuf.alloc(4 * sizeof(unsigned));
+        GL_CUDA(cudaMemsetAsync(cs.tierbuf.p, 0, 4 * sizeof(unsigned), s));
+        k_tiers<<<grid1d(n, 256, sms), 256, 0, s>>>(g, cs.tierbuf.as<unsigned>());
+        GL_LAUNCH_CHECK();
+        unsigned ht[4];
+        GL_CUDA(cudaMemcpyAsync(ht, cs.tierbuf.p, sizeof(ht), cudaMemcpyDeviceToHost, s));
+        GL_CUDA(cudaStreamSynchronize(s));
+        cs.tiers = make_uint4(ht[0], ht[1], ht[2], ht[3]);
+        cs.tiers_valid = true;
+        cs.launches += 1;
+    }
+    {
+        const char* rt = std::getenv("GL_RUN_TABLE");
+        if (m && !(rt && rt[0] == '0') && cs.runtab_key != walk_cl() + 1) {
+            const u64 S = 2 * m;
+            DevBuf rev, scan;
+            rev.alloc(S * sizeof(u32));
+            scan.alloc(S * sizeof(u32));
+            cs.runtab.alloc(S * sizeof(u64));
+            k_run_flags<<<grid1d(S, 256, sms, 16), 256, 0, s>>>(g, cs.tiers, walk_cl(), rev.as<u32>());
+            k_row_flags<<<grid1d(n, 256, sms), 256, 0, s>>>(g, rev.as<u32>());
+            GL_LAUNCH_CHECK();
+            size_t bytes = 0;
+            GL_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rev.as<u32>(), scan.as<u32>(), MinU32{},
+                                                   (int64_t)S, s));
+            cs.tmp.alloc(bytes);
+            GL_CUDA(cub::DeviceScan::InclusiveScan(cs.tmp.p, bytes, rev.as<u32>(), scan.as<u32>(), MinU32{},
+                                                   (int64_t)S, s));
+            k_run_pack<<<grid1d(S, 256, sms, 16), 256, 0, s>>>(g, scan.as<u32>(), cs.runtab.as<u64>());
+            GL_LAUNCH_CHECK();
+            GL_CUDA(cudaStreamSynchronize(s)); // rev / scan go back to the (stream-unaware) pool
+            cs.runtab_key = walk_cl() + 1;
+            cs.launches += 4;
+        }
+    }
+
     // The H-pass (stream s) and the cycle pass (cs.s2, forked after the wedge
     // prefix) are independent and run concurrently; count_mid joins them.
     if (!cs.s2) {
@@ -706,8 +759,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             // min(C(k,2), s1) per warp vertex), at most ~40% of the free memory;
             // headers in list order xl, large, medium, small
             if (!cs.tl_sized) {
-                size_t fr = 0, tot = 0;
-                GL_CUDA(cudaMemGetInfo(&fr, &tot));
+                const size_t fr = free_at_start;
                 cs.tl_cap = std::min<u64>(hc[19] / (u64)world + 1, (u64)(0.4 * (double)fr) / sizeof(uint2));
                 cs.tl_sized = true;
             }
@@ -798,8 +850,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             u32* kout = kin + (n + 1);
             u32* iin = cs.items_c.as<u32>();
             u32* iout = iin + (n + 1);
-            k_tiers<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, (unsigned*)(counters + 22));
-            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), (const unsigned*)(counters + 22),
+            k_top_keys<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, cs.wpre.as<u64>(), cs.tierbuf.as<const unsigned>(),
                                                            kin, counters + 10, counters + 15, counters + 16,
                                                            counters + 11, counters + 27, sparse_big_factor());
             k_seq<<<grid1d(n, 256, sms), 256, 0, s2>>>(iin, n);
@@ -813,7 +864,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 std::fprintf(stderr, "[gl] cycle classes sparse-big %llu big %llu mid %llu small-mid %llu small %llu\n",
                              (unsigned long long)nsparse, (unsigned long long)nbig, (unsigned long long)nmid,
                              (unsigned long long)nsmid, (unsigned long long)nsmall);
-            const uint4 tiers = make_uint4((u32)cc[22], (u32)(cc[22] >> 32), (u32)cc[23], (u32)(cc[23] >> 32));
+            const uint4 tiers = cs.tiers;
             // slot credits: u32 unless c is a hub (degree >= 65536 = ids >= tiers.w), see Credits
             const Credits credits{cs.slots.as<i64>(), cs.slots32.as<u32>(), tiers.w};
             cs.work[2] = 12 * wtot / (u64)world; // 4 B c id + 8 B slot credit per wedge
@@ -841,7 +892,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 pbig = hp[1] - hp[0];
                 cs.pieces.alloc(((u64)hp[1] * 2 + 2) * sizeof(uint4)); // all pieces, then this rank's share
                 k_pieces<<<(unsigned)std::min<u64>(nwin, (u64)sms * 8), 256, 0, s2>>>(
-                    g, cs.wpre.as<u64>(), iout, nwin, nsparse, (const unsigned*)(counters + 22), walk_cl(), poff,
+                    g, cs.wpre.as<u64>(), iout, nwin, nsparse, cs.tierbuf.as<const unsigned>(), walk_cl(), poff,
                     cs.pieces.as<uint4>());
                 GL_LAUNCH_CHECK();
                 cs.launches += 4;
@@ -871,28 +922,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                 if (mybig_p || mysparse_p) cs.cursor.alloc((u64)sms * kBigBlocksPerSM * w_big * sizeof(u32));
                 // run-end table of the dense windows (once per graph and walk_cl; GL_RUN_TABLE=0 disables)
                 const char* rt = std::getenv("GL_RUN_TABLE");
-                const bool use_runs = mybig_p && !(rt && rt[0] == '0');
-                if (use_runs && cs.runtab_key != walk_cl() + 1) {
-                    const u64 S = 2 * m;
-                    DevBuf rev, scan;
-                    rev.alloc(S * sizeof(u32));
-                    scan.alloc(S * sizeof(u32));
-                    cs.runtab.alloc(S * sizeof(u64));
-                    k_run_flags<<<grid1d(S, 256, sms, 16), 256, 0, s2>>>(g, tiers, walk_cl(), rev.as<u32>());
-                    k_row_flags<<<grid1d(n, 256, sms), 256, 0, s2>>>(g, rev.as<u32>());
-                    GL_LAUNCH_CHECK();
-                    size_t bytes = 0;
-                    GL_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rev.as<u32>(), scan.as<u32>(), MinU32{},
-                                                           (int64_t)S, s2));
-                    cs.tmp_c.alloc(bytes);
-                    GL_CUDA(cub::DeviceScan::InclusiveScan(cs.tmp_c.p, bytes, rev.as<u32>(), scan.as<u32>(),
-                                                           MinU32{}, (int64_t)S, s2));
-                    k_run_pack<<<grid1d(S, 256, sms, 16), 256, 0, s2>>>(g, scan.as<u32>(), cs.runtab.as<u64>());
-                    GL_LAUNCH_CHECK();
-                    GL_CUDA(cudaStreamSynchronize(s2)); // rev / scan go back to the (stream-unaware) pool
-                    cs.runtab_key = walk_cl() + 1;
-                    cs.launches += 4;
-                }
+                const bool use_runs = mybig_p && !(rt && rt[0] == '0') && cs.runtab_key == walk_cl() + 1;
                 if (mymid || mysmid) cs.cursor2.alloc((u64)sms * 4 * w_hash * sizeof(u32));
                 auto launch = [&](auto kind, u32* list, u64 count, u64 offset, u64 total, unsigned long long* queue) {
                     constexpr int K = decltype(kind)::value;

@@ -55,6 +55,14 @@ __device__ __forceinline__ void credit_slot(const Credits& cr, u64 slot, u32 c, 
     else
         red_add_u32_if(&cr.s32[slot], v);
 }
+// dense windows: every c of a window lies in one counter tier, and the hub ids
+// are exactly the 32-bit tier (cl == 0) -- a loop-invariant choice
+__device__ __forceinline__ void credit_slot_tier(const Credits& cr, u64 slot, u32 cl, u32 v) {
+    if (cl == 0)
+        red_add_u64_if(&cr.s64[slot], (u64)v);
+    else
+        red_add_u32_if(&cr.s32[slot], v);
+}
 
 // one-use 8-byte load (run-end table) with the same evict-first policy
 __device__ __forceinline__ u64 ld_u64_stream(const u64* p) {
@@ -413,7 +421,7 @@ __device__ __forceinline__ void wedge_op(u32* W, u32 wb, u32 cv, u32 lo, u32 cl,
         } else if (PASS == 1) {
             const u32 w = ld_shared(addr) >> sh;
             const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
-            credit_slot(cr, slot, cv, v);
+            credit_slot_tier(cr, slot, cl, v);
             val = v;
         } else {
             W[ci >> cl] = 0;
@@ -499,7 +507,7 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
                     } else if (PASS == 1) {
                         const u32 w = ld_shared(addr) >> sh;
                         const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
-                        credit_slot(cr, sbase + 32u * r, cv, v);
+                        credit_slot_tier(cr, sbase + 32u * r, cl, v);
                         acc += v;
                     } else {
                         st_shared(addr, 0u);
@@ -750,7 +758,7 @@ __device__ __noinline__ void walk_window(const DevGraph& g, const BigScratch& S,
                         const u32 ci = cv[v] - lo;
                         const u32 w = ld_shared(wb + ((ci >> cl) << 2)) >> ((ci & ((1u << cl) - 1u)) << (5 - cl));
                         const u32 val = (w & ((1u << (32u >> cl)) - 1u)) - 1u;
-                        credit_slot(cr, rb + p + v, cv[v], val);
+                        red_add_u32_if(&cr.s32[rb + p + v], val); // walk tiers: degree < 16
                         sum += val;
                     }
                 }

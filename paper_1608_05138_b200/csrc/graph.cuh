@@ -93,6 +93,9 @@ struct CountState {
     cudaStream_t s3 = nullptr;
     cudaEvent_t ev_out = nullptr;
     u32 runtab_key = 0;            // walk_cl + 1 it was built for (0: none)
+    DevBuf tierbuf;                // u32[4] degree tiers of the window counters (count.cu k_tiers)
+    uint4 tiers = {0, 0, 0, 0};
+    bool tiers_valid = false;
     cudaStream_t s2 = nullptr;     // cycle-pass stream (owned)
     cudaEvent_t ev[8] = {};        // phase events: 0/1 H-pass, 2/3 cycles, 4/5 sums, 6 fork, 7 end of count_mid
     u64 n_items2 = 0, n_items3s = 0, n_items3m = 0, n_items3b = 0, n_items3x = 0;

@@ -2,7 +2,9 @@
 //   * edge-list parsing  (load_edge_list, /root/reference/proj/src/graph.cpp:47-91)
 //   * synthetic generators (RMAT / G(n,m) / Barabasi-Albert, SPEC "cli" module)
 //   * the 128-bit count algebra (global_from_unrestricted, counts.cpp:86-111)
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -44,7 +46,12 @@ void* pool_alloc(size_t bytes, int device, size_t* got) {
         }
     }
     void* p = nullptr;
+    static const bool dbg = std::getenv("GL_DEBUG_POOL") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMalloc(&p, bytes);
+    if (dbg)
+        std::fprintf(stderr, "[gl pool] cudaMalloc %zu B: %.3f ms\n", bytes,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (e == cudaErrorMemoryAllocation) { // give the cache back and retry once
         cudaGetLastError();
         pool_trim();

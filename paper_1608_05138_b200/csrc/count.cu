@@ -761,6 +761,12 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
             if (!cs.tl_sized) {
                 const size_t fr = free_at_start;
                 cs.tl_cap = std::min<u64>(hc[19] / (u64)world + 1, (u64)(0.4 * (double)fr) / sizeof(uint2));
+                // GL_TL_EXACT=1: reserve exactly after phase 2 instead of C(k,2) up front
+                // (fills the list with more real records on large graphs, but the copy
+                // costs more than the re-derivations it saves: RMAT-24 +0.8%, RMAT-26
+                // +0.2% -- off by default)
+                const char* ex = std::getenv("GL_TL_EXACT");
+                cs.tl_exact = ex && ex[0] == '1' ? 1u : 0u;
                 cs.tl_sized = true;
             }
             cs.tlist.alloc((cs.tl_cap + 1) * sizeof(uint2));
@@ -791,7 +797,7 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                     const size_t smem = hpass_smem_bytes<kHPassCount, K>(kmax, gr.device);
                     smem_attr(k_hpass_block<kHPassCount, K>, smem, gr.device);
                     const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hbase,
-                                     cs.tl_n.as<u32>() + hbase};
+                                     cs.tl_n.as<u32>() + hbase, cs.tl_exact};
                     const bool glob = K == 1088 && cs.h_gstride;
                     k_hpass_block<kHPassCount, K><<<(unsigned)sms * HCfg<K>::MINB, HCfg<K>::THREADS, smem, s>>>(
                         g, list, count, queue, cs.t.as<u32>(), d_partials, glob ? cs.scratch.as<u32>() : nullptr,
@@ -814,7 +820,8 @@ void count_begin(Graph& gr, int rank, int world, i64* d_partials, cudaStream_t s
                                                                       cs.items3s.as<u32>());
                 GL_LAUNCH_CHECK();
                 const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20,
-                                 cs.tl_base.as<u64>() + myxl + mybig + mymedk, cs.tl_n.as<u32>() + myxl + mybig + mymedk};
+                                 cs.tl_base.as<u64>() + myxl + mybig + mymedk, cs.tl_n.as<u32>() + myxl + mybig + mymedk,
+                                 cs.tl_exact};
                 k_hpass_warp<kHPassCount><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
                     g, cs.items3s.as<u32>(), mysmall, counters + 3, cs.t.as<u32>(), d_partials, TL);
                 GL_LAUNCH_CHECK();
@@ -989,7 +996,7 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
         const size_t smem = hpass_smem_bytes<kHPassSums, K>(cs.h_kmax, gr.device);
         smem_attr(k_hpass_block<kHPassSums, K>, smem, gr.device);
         const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hbase,
-                         cs.tl_n.as<u32>() + hbase};
+                         cs.tl_n.as<u32>() + hbase, cs.tl_exact};
         const bool glob = K == 1088 && cs.h_gstride;
         k_hpass_block<kHPassSums, K><<<(unsigned)sms * HCfg<K>::MINB, HCfg<K>::THREADS, smem, s>>>(
             g, list, count, queue, cs.t.as<u32>(), d_partials, glob ? cs.scratch.as<u32>() : nullptr,
@@ -1006,7 +1013,7 @@ void count_mid(Graph& gr, i64* d_partials, cudaStream_t s) {
     if (g.m && cs.n_items3s) {
         const u64 hb = cs.n_items3x + cs.n_items3b + cs.n_items3m;
         const TriList TL{cs.tlist.as<uint2>(), cs.tl_cap, counters + 20, cs.tl_base.as<u64>() + hb,
-                         cs.tl_n.as<u32>() + hb};
+                         cs.tl_n.as<u32>() + hb, cs.tl_exact};
         k_hpass_warp<kHPassSums><<<(unsigned)sms * 8, kHWarpsPerBlock * 32, 0, s>>>(
             g, cs.items3s.as<u32>(), cs.n_items3s, counters + 6, cs.t.as<u32>(), d_partials, TL);
         GL_LAUNCH_CHECK();

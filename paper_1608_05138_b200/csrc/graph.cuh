@@ -79,6 +79,7 @@ struct CountState {
     DevBuf tlist, tl_base, tl_n; // persistent H-edge records for the triangle-sum pass
     u64 tl_cap = 0;
     bool tl_sized = false;
+    u32 tl_exact = 0;   // exact record reservations (hpass.cuh TriList::exact)
     DevBuf wpre;     // u64[m+1] wedge prefix per edge for the cycle kernels
     DevBuf items2, items3s, items3m, items3b, items3x; // work lists
     DevBuf keys, tmp, scratch, cursor, cursor2, acc; // sort keys, cub temp, kernel scratch

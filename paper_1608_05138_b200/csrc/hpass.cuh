@@ -120,6 +120,10 @@ struct TriList {
     unsigned long long* count;
     u64* base;   // per work item
     u32* n;      // per work item
+    // exact (GL_TL_EXACT=1, off by default): block vertices write their records
+    // to the block's own list and copy them in with an exact reservation after
+    // phase 2 instead of reserving C(k,2) up front
+    u32 exact;
 };
 constexpr u64 kNoList = ~0ull;
 // TriList::n flags: the low 31 bits count the records; kRecSoA marks the
@@ -431,7 +435,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // C(k,2)-record reservation (member pairs, then edge ids)
         const bool soa = TL.n[idx] & kRecSoA;
         const u32* rij = reinterpret_cast<const u32*>(rec);
-        const u32* re_ = rij + (u64)k * (k - 1) / 2;
+        const u32* re_ = rij + (TL.exact ? (u64)nrec : (u64)k * (k - 1) / 2);
         constexpr int U = 4;
         for (u32 r0 = threadIdx.x; r0 < nrec; r0 += U * blockDim.x) {
             uint2 rv[U];
@@ -499,7 +503,7 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         // reserve C(k,2) records of the device-wide list up front, so phase 1
         // appends the H-edges straight into it (no per-block copy)
         u64 b = kNoList;
-        if (TL.rec) {
+        if (TL.rec && !TL.exact) {
             const u64 need = (u64)k * (k - 1) / 2;
             b = atomicAdd(TL.count, (unsigned long long)need);
             if (b + need > TL.cap) b = kNoList;
@@ -736,6 +740,36 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
     } else {
         for (u32 i = threadIdx.x; i < k; i += blockDim.x)
             if (acc[i]) atomic_add_i64(&part[2 * (u64)g.eid[ub + i] + 1], -(i64)acc[i]);
+    }
+    if (MODE == kHPassCount && TL.rec && TL.exact) {
+        // exact reservation: copy this vertex's records from the block's list
+        // (pairs then edge ids when big, with the edge ids at offset nh)
+        __shared__ u64 s_cp;
+        const u32 nh = s_nh;
+        if (threadIdx.x == 0) {
+            u64 b = kNoList;
+            if (nh) {
+                b = atomicAdd(TL.count, (unsigned long long)nh);
+                if (b + nh > TL.cap) b = kNoList;
+            }
+            TL.base[idx] = nh ? b : 0;
+            TL.n[idx] = nh | (big ? kRecSoA : 0u);
+            s_cp = b;
+        }
+        __syncthreads();
+        const u64 b = s_cp;
+        if (nh && b != kNoList) {
+            if (big) {
+                u32* dij = reinterpret_cast<u32*>(TL.rec + b);
+                for (u32 h = threadIdx.x; h < nh; h += blockDim.x) {
+                    dij[h] = hij[h];
+                    dij[nh + h] = hee[h];
+                }
+            } else {
+                uint2* d = TL.rec + b;
+                for (u32 h = threadIdx.x; h < nh; h += blockDim.x) d[h] = hout[h];
+            }
+        }
     }
 }
 

@@ -468,3 +468,21 @@ def test_sharded_ranks_share_gpu(cuda_device, tmp_path, world, spec):
         xs.append(json.load(open(tmp_path / f"rank{r}.json"))["X"])
     assert all(x == [str(v) for v in res.X] for x in xs)
     assert np.array_equal(np.concatenate(shards), rec)
+
+
+@pytest.mark.parametrize("exact", ["1", "0"])
+def test_record_list_modes(cuda_device, monkeypatch, exact):
+    """H-edge record list filled by exact reservations after phase 2
+    (GL_TL_EXACT=1, the large-graph mode) or by C(k,2) up-front reservations
+    (=0): bit-exact either way, including the big-k path (K_1200: k = 1199 >
+    1088, records kept as SoA) and the warp / block classes (RMAT-13, BA)."""
+    monkeypatch.setenv("GL_TL_EXACT", exact)
+    for pairs in (gl.generate_rmat(13, 16, seed=21), gl.generate_ba(20000, 10, seed=4)):
+        o = Oracle(pairs)
+        X, orec = o.count(threads=THREADS, micro=True)
+        g, res, rec = gpu_count(pairs, cuda_device)
+        assert res.X == X
+        assert np.array_equal(rec, orec.view(gl.MICRO_DTYPE))
+    n = 1200
+    g, res, rec = gpu_count([(a, b) for a in range(n) for b in range(a + 1, n)], cuda_device)
+    assert res.X[7] == math.comb(n, 4) and (rec["x10"] == 0).all() and (rec["x7"] == math.comb(n - 2, 2)).all()

@@ -52,7 +52,16 @@ constexpr int kBigThreads = 1024;    // block per big top (dense windows), one b
 constexpr int kBigBlocksPerSM = 1;
 constexpr int kMidThreads = 1024;    // block per mid top (hash), one block per SM
 constexpr int kSmidThreads = 256;    // block per small-mid top (hash), four blocks per SM
-constexpr int kWindow = 32768;       // dense W window words (u32, or 2 x u16) in shared memory
+// dense W window words (flattened tiers) and run-metadata entries in shared
+// memory; GL_WINDOW_WORDS / GL_META_RUNS override at build time (A/B)
+#ifndef GL_WINDOW_WORDS
+#define GL_WINDOW_WORDS 45056
+#endif
+#ifndef GL_META_RUNS
+#define GL_META_RUNS 3072
+#endif
+constexpr int kWindow = GL_WINDOW_WORDS;
+constexpr int kMetaRuns = GL_META_RUNS;
 constexpr int kMidLog = 15;
 constexpr u32 kMidSlots = 1u << kMidLog; // mid tops: block hash, u32 keys + u16 counts (192 KB)
 constexpr u64 kMidWedges = kMidSlots / 2; // mid-top threshold (<= half the hash slots)
@@ -267,7 +276,7 @@ __device__ __forceinline__ u64 dense_windows(u32 a, const unsigned* __restrict__
     u32 prev = 0;
     for (int i = 0; i <= 4; ++i) {
         const u32 end = i < 4 ? (tiers[i] < a ? tiers[i] : a) : a;
-        const u64 span = (u64)(4 - i >= (int)kWalkCl ? (kWindow + 3 * 7168) & ~3 : kWindow) << (4 - i); // kWalkWords for walk tiers
+        const u64 span = (u64)(4 - i >= (int)kWalkCl ? (kWindow + 3 * kMetaRuns) & ~3 : kWindow) << (4 - i); // kWalkWords for walk tiers
         if (end > prev) nw += (end - prev + span - 1) / span;
         prev = end > prev ? end : prev;
     }

@@ -285,7 +285,7 @@ __device__ __forceinline__ u64 gallop_from(const u32* __restrict__ a, u64 lo, u6
 // walk_cl = the lowest counter tier that walks (default kWalkCl; 5 = never,
 // GL_WALK_CL overrides).
 constexpr u32 kWalkCl = 3;
-constexpr u32 kWalkWords = (kWindow + 3 * 7168) & ~3u; // Cyc<0>: WORDS + 3 * META (+1 unused)
+constexpr u32 kWalkWords = (kWindow + 3 * kMetaRuns) & ~3u; // Cyc<0>: WORDS + 3 * META (+1 unused)
 __host__ __device__ __forceinline__ u64 win_span(u32 cl, u64 nb, u32 walk_cl) {
     if (cl >= walk_cl) return (u64)kWalkWords << cl;
     u64 span = (u64)kWindow << cl;
@@ -352,7 +352,7 @@ template <int KIND> struct Cyc;
 template <> struct Cyc<0> {
     static constexpr bool HASH = false, WIN = true;
     static constexpr int THREADS = kBigThreads, MINB = kBigBlocksPerSM;
-    static constexpr u32 LOG = 0, WORDS = kWindow, META = 7168;
+    static constexpr u32 LOG = 0, WORDS = kWindow, META = kMetaRuns;
 };
 template <> struct Cyc<1> {
     static constexpr bool HASH = true, WIN = false;

@@ -68,9 +68,15 @@ constexpr u64 kMidWedges = kMidSlots / 2; // mid-top threshold (<= half the hash
 constexpr int kSmidLog = 13;
 // sparse big tops (windowed block hash): c windows sized for ~kHashWinTarget
 // wedges, re-cut when a window holds more than kHashWinMax (and spans more
-// than kHashWinMax ids), so a window's distinct c ids stay <= 5/8 of the slots
-constexpr u32 kHashWinTarget = 12288;
-constexpr u32 kHashWinMax = 20480;
+// than kHashWinMax ids), so a window's distinct c ids stay <= kHashWinMax =
+// 27306 of the 32768 slots (load <= 83%; 16384 measured faster than round 1's
+// 12288 / 20480: BA cycles -1%, RMAT-24 -1.7%; 8192 slower)
+#ifndef GL_HASH_WIN
+#define GL_HASH_WIN 16384
+#endif
+static_assert(GL_HASH_WIN * 5 / 3 < (1 << 15), "windowed hash: distinct ids must stay below the slot count");
+constexpr u32 kHashWinTarget = GL_HASH_WIN;
+constexpr u32 kHashWinMax = GL_HASH_WIN * 5 / 3;
 constexpr u64 kSmidWedges = (1u << kSmidLog) / 2; // small-mid threshold
 
 constexpr u32 kEmpty = 0xffffffffu;

@@ -186,19 +186,19 @@ def test_sparse_big_windowed_hash(cuda_device, monkeypatch, mode, n, k, seed):
 
 
 def recut_graph(seed=1):
-    """Top A (degree 300) over 100 b's whose wedges crowd the low end of a wide
-    c range: 1100 ids of degree 20 (C1) adjacent to 20 b's each hold 22000
-    wedges, then 58900 ids of degree 20-21 (a circulant C2, 3000 of them with
-    one b) hold 3000.  A's first windowed-hash window (~29K ids by the
-    uniform estimate) holds ~23K wedges > kHashWinMax and is re-cut."""
+    """Top A (degree 500) over 100 b's (degree ~331) whose wedges crowd the low
+    end of a wide c range: 1500 ids of degree 20 (C1) adjacent to 20 b's each
+    hold 30000 wedges, then 58500 ids of degree 20-21 (a circulant C2, 3000 of
+    them with one b) hold 3000.  A's first windowed-hash window (~30K ids by the
+    uniform estimate) holds ~30K wedges > kHashWinMax (27306) and is re-cut."""
     rng = np.random.default_rng(seed)
-    nb, n1, n2 = 100, 1100, 58900
+    nb, n1, n2 = 100, 1500, 58500
     A = 0
     bs = np.arange(1, 1 + nb)
     c1 = np.arange(1 + nb, 1 + nb + n1)
     c2 = np.arange(1 + nb + n1, 1 + nb + n1 + n2)
-    leaves = np.arange(c2[-1] + 1, c2[-1] + 1 + 200)
-    e = [np.stack([np.full(nb, A), bs], 1), np.stack([np.full(200, A), leaves], 1)]
+    leaves = np.arange(c2[-1] + 1, c2[-1] + 1 + 400)
+    e = [np.stack([np.full(nb, A), bs], 1), np.stack([np.full(400, A), leaves], 1)]
     for c in c1:
         e.append(np.stack([rng.choice(bs, 20, replace=False), np.full(20, c)], 1))
     i = np.arange(n2)

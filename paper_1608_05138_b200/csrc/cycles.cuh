@@ -595,9 +595,15 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
 // Guided self-scheduling of a window pass: a warp grabs about 1/(2*nwarps) of
 // the wedges still unclaimed (at most 8192, at least 64), so the grabs shrink
 // towards the end of the pass and the block's barrier waits for a short tail.
+#ifndef GL_GRAB_DIV
+#define GL_GRAB_DIV 2
+#endif
+#ifndef GL_GRAB_MAX
+#define GL_GRAB_MAX 8192
+#endif
 __device__ __forceinline__ u32 grab_size(u32 remaining, u32 nwarps) {
-    u32 g = remaining / (2u * nwarps);
-    g = g < 8192u ? g : 8192u;
+    u32 g = remaining / (GL_GRAB_DIV * nwarps);
+    g = g < (u32)GL_GRAB_MAX ? g : (u32)GL_GRAB_MAX;
     g = (g + 31u) & ~31u;
     return g > 64u ? g : 64u;
 }

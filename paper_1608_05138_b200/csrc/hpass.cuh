@@ -30,7 +30,10 @@
 constexpr int kHPassCount = 0, kHPassSums = 1;
 constexpr int kHWarpMax = 32;       // 2 <= k <= 32: one warp, one u32 row per lane
 constexpr int kHWarpsPerBlock = 8;
-constexpr int kHUnroll = 8;         // streamed rounds in flight per warp
+#ifndef GL_HUNROLL
+#define GL_HUNROLL 8
+#endif
+constexpr int kHUnroll = GL_HUNROLL; // streamed rounds in flight per warp
 constexpr u32 kHProbeRatio = 16;    // probe instead of stream when |U(x_i)| > 16 * candidates (8: RMAT-24 H-pass +2.5%)
 __constant__ u32 c_probe_ratio = kHProbeRatio; // GL_PROBE_RATIO overrides (tuning experiments)
 
@@ -51,7 +54,10 @@ template <int BLOG> __host__ __device__ constexpr u32 bloom_words() { return (1u
 // fixed per-vertex latency of the many small vertices overlaps across blocks)
 template <int KMAX> struct HCfg;
 template <> struct HCfg<1088> { static constexpr int THREADS = 1024, MINB = 1, BLOG = 16; };
-template <> struct HCfg<768> { static constexpr int THREADS = 512, MINB = 2, BLOG = 16; };
+#ifndef GL_BLOG768
+#define GL_BLOG768 16
+#endif
+template <> struct HCfg<768> { static constexpr int THREADS = 512, MINB = 2, BLOG = GL_BLOG768; };
 template <> struct HCfg<128> { static constexpr int THREADS = 128, MINB = 8, BLOG = 13; };
 
 __device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 2k, >= 64 (Bloom filters the misses)

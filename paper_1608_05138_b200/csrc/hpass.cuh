@@ -58,7 +58,10 @@ template <> struct HCfg<1088> { static constexpr int THREADS = 1024, MINB = 1, B
 #define GL_BLOG768 16
 #endif
 template <> struct HCfg<768> { static constexpr int THREADS = 512, MINB = 2, BLOG = GL_BLOG768; };
-template <> struct HCfg<128> { static constexpr int THREADS = 128, MINB = 8, BLOG = 13; };
+#ifndef GL_H128_THREADS
+#define GL_H128_THREADS 128
+#endif
+template <> struct HCfg<128> { static constexpr int THREADS = GL_H128_THREADS, MINB = 1024 / GL_H128_THREADS, BLOG = 13; };
 
 __device__ __forceinline__ u32 hp_log(u32 k) { // hash slots 2^log >= 2k, >= 64 (Bloom filters the misses)
     u32 l = 32 - __clz(2 * k - 1);

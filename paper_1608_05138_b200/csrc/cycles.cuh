@@ -472,6 +472,8 @@ __device__ __forceinline__ u32 warp_upper_bound(const u32* a, u32 n, u32 x) {
 #endif
 constexpr int kUnroll = GL_KUNROLL; // uniform-path rounds with loads in flight per lane (12: -1..2% vs 8 or 16)
 
+template <bool B> struct HubTag { static constexpr bool v = B; };
+
 template <int KIND, int PASS>
 __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S, u32 nnz, u32 kb, u32 ke, u32* W,
                                             u32 lo, u32 cl, u64 abase, Credits cr) {
@@ -490,58 +492,99 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
 #ifdef GL_CYCLE_PROF_ROUNDS
             if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[12], (unsigned long long)nfull);
 #endif
-            const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
-            u64 acc = 0;
-            // every round of the stretch is full: branch-free wedge ops on a
-            // hoisted shared base (dense windows), groups of kHalf rounds with
-            // the next group's loads in flight, then up to kHalf-1 tail rounds
-            constexpr int kHalf = kUnroll / 2;
-            const u32* __restrict__ src = g.adj + sbase;
-            auto op = [&](u32 cv, u32 r) {
-                if constexpr (!Cyc<KIND>::HASH) {
-                    const u32 ci = cv - lo;
-                    const u32 addr = wb + ((ci >> cl) << 2);
-                    const u32 sh = (ci & ((1u << cl) - 1u)) << (5 - cl);
-                    if (PASS == 0) {
-                        red_shared_add(addr, 1u << sh);
-                    } else if (PASS == 1) {
-                        const u32 w = ld_shared(addr) >> sh;
-                        const u32 v = (cl == 0 ? w : w & ((1u << (32u >> cl)) - 1u)) - 1u;
-                        credit_slot_tier(cr, sbase + 32u * r, cl, v);
-                        acc += v;
+            // dense windows: the counter tier's hub/non-hub credit choice is
+            // taken once per stretch, not per wedge
+            auto stretch = [&](auto hubc) {
+                constexpr bool HUB = decltype(hubc)::v;
+                const u64 sbase = (u64)S.rs[bs] + (k0 - S.pre[bs]) + lane;
+                u64 acc = 0;
+                // every round of the stretch is full: branch-free wedge ops on a
+                // hoisted shared base (dense windows), groups of kHalf rounds with
+                // the next group's loads in flight; the last group overlaps the
+                // (predicated) loads of the < kHalf tail rounds
+                constexpr int kHalf = kUnroll / 2;
+                const u32* __restrict__ src = g.adj + sbase;
+                auto op = [&](u32 cv, u32 r) {
+                    if constexpr (!Cyc<KIND>::HASH && HUB) {
+                        const u32 addr = wb + ((cv - lo) << 2);
+                        if (PASS == 0) {
+                            red_shared_add(addr, 1u);
+                        } else if (PASS == 1) {
+                            const u32 v = ld_shared(addr) - 1u;
+                            red_add_u64_if(&cr.s64[sbase + 32u * r], (u64)v);
+                            acc += v;
+                        } else {
+                            st_shared(addr, 0u);
+                        }
+                    } else if constexpr (!Cyc<KIND>::HASH) {
+                        const u32 ci = cv - lo;
+                        const u32 addr = wb + ((ci >> cl) << 2);
+                        const u32 sh = (ci & ((1u << cl) - 1u)) << (5 - cl);
+                        if (PASS == 0) {
+                            red_shared_add(addr, 1u << sh);
+                        } else if (PASS == 1) {
+                            const u32 w = ld_shared(addr) >> sh;
+                            const u32 v = (w & ((1u << (32u >> cl)) - 1u)) - 1u; // cl >= 1 here
+                            red_add_u32_if(&cr.s32[sbase + 32u * r], v);
+                            acc += v;
+                        } else {
+                            st_shared(addr, 0u);
+                        }
                     } else {
-                        st_shared(addr, 0u);
+                        u64 v = 0;
+                        wedge_op<KIND, PASS>(W, wb, cv, lo, cl, cr, sbase + 32u * r, v);
+                        acc += v;
                     }
-                } else {
-                    u64 v = 0;
-                    wedge_op<KIND, PASS>(W, wb, cv, lo, cl, cr, sbase + 32u * r, v);
-                    acc += v;
-                }
-            };
-            u32 r = 0;
-            if (nfull >= (u32)kHalf) {
-                u32 cv[kHalf];
+                };
+                u32 r = 0;
+                if (nfull >= (u32)kHalf) {
+                    u32 cv[kHalf];
 #pragma unroll
-                for (int u = 0; u < kHalf; ++u) cv[u] = __ldg(src + 32u * u);
-                for (; r + 2 * kHalf <= nfull; r += kHalf) {
-                    u32 nx[kHalf];
+                    for (int u = 0; u < kHalf; ++u) cv[u] = __ldg(src + 32u * u);
+                    for (; r + 2 * kHalf <= nfull; r += kHalf) {
+                        u32 nx[kHalf];
 #pragma unroll
-                    for (int u = 0; u < kHalf; ++u) nx[u] = __ldg(src + 32u * (r + kHalf + u));
+                        for (int u = 0; u < kHalf; ++u) nx[u] = __ldg(src + 32u * (r + kHalf + u));
+#pragma unroll
+                        for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
+#pragma unroll
+                        for (int u = 0; u < kHalf; ++u) cv[u] = nx[u];
+                    }
+                    // the final group with the < kHalf tail rounds' loads in flight
+                    u32 tl[kHalf];
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u) tl[u] = r + kHalf + u < nfull ? __ldg(src + 32u * (r + kHalf + u)) : 0u;
 #pragma unroll
                     for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
+                    r += kHalf;
 #pragma unroll
-                    for (int u = 0; u < kHalf; ++u) cv[u] = nx[u];
+                    for (int u = 0; u < kHalf; ++u)
+                        if (r + u < nfull) op(tl[u], r + u);
+                    r = nfull;
                 }
+                // the < kHalf remaining rounds: all loads in flight, then the ops
+                if (r < nfull) {
+                    u32 cv[kHalf];
 #pragma unroll
-                for (int u = 0; u < kHalf; ++u) op(cv[u], r + u);
-                r += kHalf;
+                    for (int u = 0; u < kHalf; ++u) cv[u] = r + u < nfull ? __ldg(src + 32u * (r + u)) : 0u;
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u)
+                        if (r + u < nfull) op(cv[u], r + u);
+                }
+                if (PASS == 1) {
+                    acc = warp_sum_u64(acc);
+                    if (lane == 0 && acc) atomic_add_i64(&cr.s64[abase + S.rj[bs]], (i64)acc);
+                }
+                k0 += nfull << 5;
+            };
+            if constexpr (Cyc<KIND>::HASH) {
+                stretch(HubTag<false>{});
+            } else {
+                if (cl == 0)
+                    stretch(HubTag<true>{});
+                else
+                    stretch(HubTag<false>{});
             }
-            for (; r < nfull; ++r) op(__ldg(src + 32u * r), r);
-            if (PASS == 1) {
-                acc = warp_sum_u64(acc);
-                if (lane == 0 && acc) atomic_add_i64(&cr.s64[abase + S.rj[bs]], (i64)acc);
-            }
-            k0 += nfull << 5;
         } else {
             // mixed round [k0, k0 + 32): runs bs, bs+1, ... start at pre[bs+j];
             // one OR-reduction gives the bitmask of run starts inside the round,

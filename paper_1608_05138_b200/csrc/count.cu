@@ -32,6 +32,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -507,14 +508,15 @@ __global__ void k_run_pack(DevGraph g, const u32* __restrict__ scan, u64* __rest
     }
 }
 
-// Piece cap: no work item above 1/4 of one SM's fair share of the job,
-// wedges / (4 * SMs * ranks) (at least 2^17): 1/592 of the cycle work on one
-// B200, 1/4736 at 8 ranks.  GL_PIECE_WEDGES=<n> overrides it (and lowers the
-// wedges-per-b floor to 1), so tests force splitting on small graphs.
+// lowest counter tier of the thread-walk windows (cycles.cuh, kWalkCl)
 inline u32 walk_cl() {
     const char* e = std::getenv("GL_WALK_CL");
     return e && *e >= '0' && *e <= '9' ? (u32)std::strtoul(e, nullptr, 10) : kWalkCl;
 }
+// Piece cap: no work item above 1/4 of one SM's fair share of the job,
+// wedges / (4 * SMs * ranks) (at least 2^17): 1/592 of the cycle work on one
+// B200, 1/4736 at 8 ranks.  GL_PIECE_WEDGES=<n> overrides it (and lowers the
+// wedges-per-b floor to 1), so tests force splitting on small graphs.
 inline bool piece_forced() {
     const char* e = std::getenv("GL_PIECE_WEDGES");
     return e && *e >= '0' && *e <= '9';
@@ -560,13 +562,18 @@ void dev_sort_desc(DevBuf& tmp, u32* keys_in, u32* keys_out, u32* ids_in, u32* i
 // hpass_vertex rows_g), minus the kernel's static shared memory.
 template <int MODE, int K> size_t hpass_smem_bytes(u32 kmax, int device);
 
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) raised to the largest size
+// requested so far per (kernel, device): the attribute is a limit, and a graph
+// that needs less must not lower it under a later graph that needs more
 template <typename K> void smem_attr(K* kernel, size_t smem, int device) {
     static std::mutex mu;
-    static std::set<std::tuple<const void*, int, size_t>> done;
+    static std::map<std::pair<const void*, int>, size_t> set_to;
     std::lock_guard<std::mutex> lk(mu);
-    if (done.insert({reinterpret_cast<const void*>(kernel), device, smem}).second)
+    size_t& cur = set_to[{reinterpret_cast<const void*>(kernel), device}];
+    if (smem > cur) {
         GL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cur = smem;
+    }
 }
 
 template <int MODE, int K> size_t hpass_smem_bytes(u32 kmax, int device) {

@@ -277,14 +277,15 @@ __device__ __forceinline__ u64 gallop_from(const u32* __restrict__ a, u64 lo, u6
 // t0 + i * span.  span keeps nb * span < 2^31 (window wedge counts and indices
 // are u32).  A fixed grid lets a top's c-range pieces cut on window boundaries
 // (the pieces then hold exactly the windows of the unsplit top).
-// Windows over the low-degree tiers (cl >= kWalkCl: degree < 16, 2- and 4-bit
-// counters) hold short runs (RMAT-24: 2.5 / 5 wedges per run, half of all
-// windows and 42% of the runs for 5.5% of the wedges): there each thread walks
-// its b's runs itself (no run search, no scan, no flattening) and the window
-// spans the whole dynamic shared memory (the run metadata is not needed).
-// walk_cl = the lowest counter tier that walks (default kWalkCl; 5 = never,
-// GL_WALK_CL overrides).
-constexpr u32 kWalkCl = 3;
+// Windows over the lowest-degree tier (cl >= kWalkCl = 4: 2-bit counters,
+// degree < 4) hold short runs (RMAT-24: 6.4 wedges per run, 24% of the windows
+// for 1.6% of the wedges): there each thread walks its b's runs itself (no run
+// search, no scan, no flattening) and the window spans the whole dynamic
+// shared memory (the run metadata is not needed).  The 4-bit tier walked too
+// until the flattened mixed rounds went two at a time (measured: RMAT-20
+// cycles -3% flattened, RMAT-24 +0.8%).  walk_cl = the lowest counter tier that
+// walks (default kWalkCl; 5 = never, GL_WALK_CL overrides).
+constexpr u32 kWalkCl = 4;
 constexpr u32 kWalkWords = (kWindow + 3 * kMetaRuns) & ~3u; // Cyc<0>: WORDS + 3 * META (+1 unused)
 __host__ __device__ __forceinline__ u64 win_span(u32 cl, u64 nb, u32 walk_cl) {
     if (cl >= walk_cl) return (u64)kWalkWords << cl;
@@ -593,44 +594,69 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
 #ifdef GL_CYCLE_PROF_ROUNDS
             if (KIND == 0 && PASS == 1 && lane_id() == 0) atomicAdd(&g_cycle_prof[13], 1ull);
 #endif
-            const u32 k = k0 + lane;
-            const bool valid = k < ke;
-            const u32 pi = bs + lane <= nnz ? S.pre[bs + lane] : 0xffffffffu;
-            const u32 rel = pi - k0; // >= 1 for lanes >= 1 (pre strictly increasing)
-            const u32 starts = __reduce_or_sync(0xffffffffu, (lane > 0 && rel < 32u) ? 1u << rel : 0u);
-            const u32 le = starts & (0xffffffffu >> (31 - lane)); // starts at or below this lane
-            const u32 owner = __popc(le);
-            const u32 q = bs + owner;
-            const u32 seg0 = owner ? 31u - __clz(le) : 0u;
-            const u32 pi0 = __shfl_sync(0xffffffffu, pi, 0); // all lanes: full-mask shuffle
-            const u32 off = owner ? lane - seg0 : k - pi0;
-            u64 v = 0;
-            if (valid) {
-                const u64 slot = (u64)S.rs[q] + off;
-                wedge_op<KIND, PASS>(W, wb, __ldg(g.adj + slot), lo, cl, cr, slot, v);
-            }
-            if (PASS == 1) {
-                const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));
-                if (cl) {
-                    // counters of <= 16 bits: the segment sum fits u32
-                    u32 v32 = (u32)v;
+            // two rounds per step when the warp's range allows: both rounds'
+            // lanes mapped to (run, slot) and both adjacency loads in flight
+            // before either round's wedge ops.
+            auto map = [&](u32 r0, u32 b0, u32& starts, u32& seg0, u32& q, u32& off) {
+                const u32 pi = b0 + lane <= nnz ? S.pre[b0 + lane] : 0xffffffffu;
+                const u32 rel = pi - r0; // >= 1 for lanes >= 1 (b0 holds wedge r0)
+                starts = __reduce_or_sync(0xffffffffu, (lane > 0 && rel < 32u) ? 1u << rel : 0u);
+                const u32 le = starts & (0xffffffffu >> (31 - lane));
+                const u32 owner = __popc(le);
+                q = b0 + owner;
+                seg0 = owner ? 31u - __clz(le) : 0u;
+                const u32 pi0 = __shfl_sync(0xffffffffu, pi, 0);
+                off = owner ? lane - seg0 : r0 + lane - pi0;
+            };
+            auto finish = [&](u32 r0, u32 starts, u32 seg0, u32 q, u64 slot, u32 cv) {
+                const u32 k = r0 + lane;
+                const bool valid = k < ke;
+                u64 v = 0;
+                if (valid) wedge_op<KIND, PASS>(W, wb, cv, lo, cl, cr, slot, v);
+                if (PASS == 1) {
+                    const bool tail = valid && (lane == 31 || k + 1 == ke || ((starts >> (lane + 1)) & 1u));
+                    if (cl) {
+                        u32 v32 = (u32)v;
 #pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const u32 t = __shfl_up_sync(0xffffffffu, v32, d);
-                        if (lane >= seg0 + (u32)d) v32 += t;
-                    }
-                    if (tail && v32) atomic_add_i64(&cr.s64[abase + S.rj[q]], (i64)v32);
-                } else {
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const u32 t = __shfl_up_sync(0xffffffffu, v32, d);
+                            if (lane >= seg0 + (u32)d) v32 += t;
+                        }
+                        if (tail && v32) atomic_add_i64(&cr.s64[abase + S.rj[q]], (i64)v32);
+                    } else {
 #pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const u64 t = __shfl_up_sync(0xffffffffu, v, d);
-                        if (lane >= seg0 + (u32)d) v += t;
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const u64 t = __shfl_up_sync(0xffffffffu, v, d);
+                            if (lane >= seg0 + (u32)d) v += t;
+                        }
+                        if (tail && v) atomic_add_i64(&cr.s64[abase + S.rj[q]], (i64)v);
                     }
-                    if (tail && v) atomic_add_i64(&cr.s64[abase + S.rj[q]], (i64)v);
                 }
+            };
+            u32 st1, sg1, q1, of1;
+            map(k0, bs, st1, sg1, q1, of1);
+            const bool v1 = k0 + lane < ke;
+            const u64 sl1 = v1 ? (u64)S.rs[q1] + of1 : 0ull;
+            const u32 c1 = v1 ? __ldg(g.adj + sl1) : 0u;
+            u32 bs2 = __shfl_sync(0xffffffffu, q1, 31);
+            if (k0 + 32u < ke) {
+                // the run holding wedge k0 + 32: the last round's, or the next
+                // when that one ends at the boundary (a round sees 31 starts)
+                bs2 += S.pre[bs2 + 1] <= k0 + 32u ? 1u : 0u;
+                u32 st2, sg2, q2, of2;
+                map(k0 + 32u, bs2, st2, sg2, q2, of2);
+                const bool v2 = k0 + 32u + lane < ke;
+                const u64 sl2 = v2 ? (u64)S.rs[q2] + of2 : 0ull;
+                const u32 c2 = v2 ? __ldg(g.adj + sl2) : 0u;
+                finish(k0, st1, sg1, q1, sl1, c1);
+                finish(k0 + 32u, st2, sg2, q2, sl2, c2);
+                k0 += 64;
+                bs = __shfl_sync(0xffffffffu, q2, 31);
+            } else {
+                finish(k0, st1, sg1, q1, sl1, c1);
+                k0 += 32;
+                bs = bs2;
             }
-            k0 += 32;
-            bs = __shfl_sync(0xffffffffu, q, 31);
         }
     }
 }

@@ -138,6 +138,18 @@ def test_complete_graphs_closed_form(cuda_device, n):
     assert (rec["t"] == n - 2).all() and (rec["x7"] == math.comb(n - 2, 2)).all() and (rec["x10"] == 0).all()
 
 
+def test_hpass_smem_limit_across_graphs(cuda_device):
+    """The xl H-pass kernel's dynamic shared-memory limit is a per-process
+    attribute: a graph needing less (K_800, xl class in shared memory) must
+    not lower it under a later graph needing more (K_1200, the whole opt-in
+    size).  The round-2 regression: K_1200 -> K_800 -> K_1200 failed its
+    last launch with 'invalid argument'."""
+    for n in (1200, 800, 1200):
+        pairs = [(a, b) for a in range(n) for b in range(a + 1, n)]
+        g, res, rec = gpu_count(pairs, cuda_device)
+        assert res.X[7] == math.comb(n, 4) and (rec["t"] == n - 2).all()
+
+
 def test_cycles_and_stars_closed_form(cuda_device):
     for n in (5, 9, 100):
         g, res, rec = gpu_count([(i, (i + 1) % n) for i in range(n)], cuda_device)

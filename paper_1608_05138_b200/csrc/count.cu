@@ -523,7 +523,9 @@ inline bool piece_forced() {
 }
 inline u64 piece_cap(u64 wtot, int sms, int world) {
     if (piece_forced()) return std::max<u64>(1, std::strtoull(std::getenv("GL_PIECE_WEDGES"), nullptr, 10));
-    return std::max<u64>(wtot / (4ull * (u64)sms * (u64)world), 1ull << 17);
+    const char* e = std::getenv("GL_PIECE_DIV"); // A/B knob for the per-SM share divisor
+    const u64 div = e && *e >= '1' && *e <= '9' ? std::strtoull(e, nullptr, 10) : 4ull;
+    return std::max<u64>(wtot / (div * (u64)sms * (u64)world), 1ull << 17);
 }
 
 struct Timer {

@@ -445,7 +445,10 @@ __device__ __forceinline__ void hpass_vertex(const DevGraph& g, u32* __restrict_
         const bool soa = TL.n[idx] & kRecSoA;
         const u32* rij = reinterpret_cast<const u32*>(rec);
         const u32* re_ = rij + (TL.exact ? (u64)nrec : (u64)k * (k - 1) / 2);
-        constexpr int U = 4;
+#ifndef GL_SUMS_U
+#define GL_SUMS_U 4
+#endif
+        constexpr int U = GL_SUMS_U; // records in flight per thread
         for (u32 r0 = threadIdx.x; r0 < nrec; r0 += U * blockDim.x) {
             uint2 rv[U];
             u32 tv[U];

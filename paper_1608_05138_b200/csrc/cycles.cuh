@@ -485,7 +485,8 @@ __device__ __forceinline__ void window_pass(const DevGraph& g, const RunMeta& S,
     u32 k0 = kb;
     while (k0 < ke) {
         u32 e1 = S.pre[bs + 1];
-        while (e1 <= k0) e1 = S.pre[++bs + 1];
+        // bs holds wedge k0 - 1 or k0: runs are non-empty, so one step
+        if (e1 <= k0) e1 = S.pre[++bs + 1];
         const u32 stop = e1 < ke ? e1 : ke;
         if (stop - k0 >= 32u) {
             // uniform stretch of full rounds inside run bs

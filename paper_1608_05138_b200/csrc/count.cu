@@ -511,7 +511,8 @@ __global__ void k_run_pack(DevGraph g, const u32* __restrict__ scan, u64* __rest
 // lowest counter tier of the thread-walk windows (cycles.cuh, kWalkCl)
 inline u32 walk_cl() {
     const char* e = std::getenv("GL_WALK_CL");
-    return e && *e >= '0' && *e <= '9' ? (u32)std::strtoul(e, nullptr, 10) : kWalkCl;
+    // >= 1: the walk credits slots in 32 bits, never valid for the hub tier (cl 0)
+    return e && *e >= '1' && *e <= '9' ? (u32)std::strtoul(e, nullptr, 10) : kWalkCl;
 }
 // Piece cap: no work item above 1/4 of one SM's fair share of the job,
 // wedges / (4 * SMs * ranks) (at least 2^17): 1/592 of the cycle work on one

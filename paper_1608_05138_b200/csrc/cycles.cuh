@@ -834,7 +834,7 @@ __device__ __noinline__ void walk_window(const DevGraph& g, const BigScratch& S,
                         const u32 ci = cv[v] - lo;
                         const u32 w = ld_shared(wb + ((ci >> cl) << 2)) >> ((ci & ((1u << cl) - 1u)) << (5 - cl));
                         const u32 val = (w & ((1u << (32u >> cl)) - 1u)) - 1u;
-                        red_add_u32_if(&cr.s32[rb + p + v], val); // walk tiers: degree < 16
+                        red_add_u32_if(&cr.s32[rb + p + v], val); // walk tiers: cl >= 1, never the hub tier
                         sum += val;
                     }
                 }

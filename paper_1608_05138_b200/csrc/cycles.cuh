@@ -461,11 +461,12 @@ __device__ __forceinline__ u32 warp_upper_bound(const u32* a, u32 n, u32 x) {
 // One pass over a warp's range [kb, ke) of a window's flattened wedge list
 // (compacted runs q, S.pre = wedge prefix, run q = adjacency slots
 // [S.rs[q], S.rs[q] + len)).  Stretches of full 32-wedge rounds inside one
-// run take the uniform path: slot = base + lane, four rounds of loads in
+// run take the uniform path: slot = base + lane, kUnroll/2 rounds of loads in
 // flight, the (a,b) credit kept per lane and warp-reduced once per stretch.
-// Rounds that straddle runs take the mixed path: each lane finds its run
-// among the next 32 starts by a 5-step shuffle search and the (a,b) credit is
-// a segmented shuffle sum whose tail lanes issue the RED.
+// Rounds that straddle runs take the mixed path, two rounds per step: each
+// lane finds its run from one OR-reduction of the run starts in its round,
+// both rounds' adjacency loads are issued before either round's ops, and the
+// (a,b) credit is a segmented shuffle sum whose tail lanes issue the RED.
 //   PASS 0: W[c]++     PASS 1: credit W[c]-1 to (b,c) and, summed, to (a,b)
 //   PASS 2: W[c] = 0 (sparse clear of a dense window)
 #ifndef GL_KUNROLL
